@@ -1,0 +1,139 @@
+/*
+ * radial_cuda.h -- C-ABI of the B200-native radial attention hot path.
+ *
+ * Plain pointers, sizes and an opaque layout handle; no C++ or torch types.
+ * Each entry point names the reference interface it replaces
+ * (/root/reference/proj/include/radial/...).  The C++ drop-in headers under
+ * include/radial/ re-expose the reference's names on top of this ABI, and
+ * INTEGRATION.md shows the ctypes / C++ bindings a maintainer would add.
+ *
+ * Conventions
+ *  - Return value: RADIAL_OK (0) or one of the RADIAL_ERR_* codes below;
+ *    radial_cuda_last_error() returns the thread-local message of the last
+ *    failure on the calling thread (reference exception text where one
+ *    exists, e.g. "masked_attention: query row 0 keeps no keys").
+ *  - Device tensors are bf16 [heads][n][head_dim], row-major, contiguous;
+ *    lse is fp32 [heads][n] (natural log of the softmax partition).
+ *  - `stream` is a cudaStream_t passed as void* (NULL = legacy stream).
+ *    Device-pointer calls are asynchronous on that stream; host-pointer calls
+ *    synchronise before returning.
+ *  - Reentrant per stream.  Layout handles are immutable after build and may
+ *    be shared by any number of streams on their device.
+ */
+#ifndef RADIAL_CUDA_H
+#define RADIAL_CUDA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RADIAL_CUDA_ABI_VERSION 1
+
+enum radial_status {
+    RADIAL_OK = 0,
+    RADIAL_ERR_INVALID = 1,   /* std::invalid_argument in the reference */
+    RADIAL_ERR_EMPTY_ROW = 2, /* std::runtime_error "query row u keeps no keys" (attention.hpp:255-258) */
+    RADIAL_ERR_CUDA = 3,      /* CUDA runtime / driver failure */
+    RADIAL_ERR_OOM = 4,       /* device allocation failed */
+    RADIAL_ERR_LENGTH = 5     /* std::length_error (block grid > 2^32 rows, block.hpp:50-52) */
+};
+
+/* PatternKind u8 values (grid.hpp:44-52). */
+enum radial_kind {
+    RADIAL_KIND_RADIAL = 0,
+    RADIAL_KIND_DENSE = 1,
+    RADIAL_KIND_SPATIAL = 2,
+    RADIAL_KIND_TEMPORAL = 3,
+    RADIAL_KIND_STA = 4,
+    RADIAL_KIND_POWER = 5,
+    RADIAL_KIND_HARMONIC = 6
+};
+
+typedef struct radial_layout radial_layout; /* opaque device-resident block layout */
+
+typedef struct radial_layout_info {
+    uint32_t frames, tokens_per_frame, block_size, grid_rows;
+    uint8_t kind, sink;
+    uint64_t kept_blocks;   /* nnz of the CSR */
+    int64_t first_empty_row; /* first block row with no kept block, -1 if none */
+    uint32_t max_row_len, min_row_len;
+} radial_layout_info;
+
+int radial_cuda_abi_version(void);
+const char* radial_cuda_last_error(void);
+
+/* ---- mask construction: replaces radial::blockify(GridShape, PatternSpec, B)
+ *      (block.hpp:59-120, keep rule mask.hpp:105-154).  Builds the CSR
+ *      (bit-exact with the reference), its transpose and the kernel work lists
+ *      on the device.  temporal_window / spatial_window are read only by the
+ *      kinds that need them (grid.hpp:83-139). */
+int radial_cuda_mask_build(uint32_t frames, uint32_t tokens_per_frame, uint32_t block_size,
+                           int kind, int sink, uint32_t temporal_window,
+                           uint32_t spatial_window, void* stream, radial_layout** out);
+
+/* Uploads a host CSR (e.g. from radial::deserialize, block.hpp:239-307) and
+ * builds the device work lists for it.  Validates the CSR like deserialize. */
+int radial_cuda_layout_from_csr(uint32_t frames, uint32_t tokens_per_frame, uint32_t block_size,
+                                int kind, int sink, uint32_t grid_rows, const uint64_t* row_ptr,
+                                const uint32_t* col_idx, void* stream, radial_layout** out);
+
+int radial_cuda_layout_info(const radial_layout* layout, radial_layout_info* info);
+
+/* D2H copy of the CSR: row_ptr u64[grid_rows+1], col_idx u32[kept_blocks]
+ * (BlockLayout::row_ptr / col_idx, block.hpp:23-45).  Synchronous. */
+int radial_cuda_layout_copy_csr(const radial_layout* layout, uint64_t* row_ptr, uint32_t* col_idx);
+
+/* D2H copy of the transpose (per-KV-block query-block lists, used by the
+ * backward): col_ptr u64[grid_rows+1], row_idx u32[kept_blocks]. */
+int radial_cuda_layout_copy_csc(const radial_layout* layout, uint64_t* col_ptr, uint32_t* row_idx);
+
+/* Device pointers of the CSR (valid for the handle's lifetime). */
+int radial_cuda_layout_device_csr(const radial_layout* layout, const uint64_t** row_ptr,
+                                  const uint32_t** col_idx);
+
+void radial_cuda_layout_free(radial_layout* layout);
+
+/* ---- sparse forward: replaces radial::masked_attention(const AttentionInstance&,
+ *      const BlockLayout&) (attention.hpp:229-270) for all heads at once.
+ *      head_dim in {64,128}, block_size in {64,128}; scale <= 0 means 1/sqrt(head_dim)
+ *      (attention.hpp:130).  lse may be NULL. */
+int radial_cuda_attn_fwd(const void* q, const void* k, const void* v, void* o, float* lse,
+                         uint32_t heads, uint64_t n, uint32_t head_dim, float scale,
+                         const radial_layout* layout, void* stream);
+
+/* ---- dense comparator: replaces radial::dense_attention (attention.hpp:141-163),
+ *      same kernel over every KV block; block_size picks the KV tile (64/128). */
+int radial_cuda_attn_fwd_dense(const void* q, const void* k, const void* v, void* o, float* lse,
+                               uint32_t heads, uint64_t n, uint32_t head_dim, uint32_t block_size,
+                               float scale, void* stream);
+
+/* ---- host-buffer forward (the reference call shape: host data in, host data
+ *      out).  q/k/v/o are bf16 [heads][n][head_dim] in host memory (pinned or
+ *      pageable); copies H2D, runs radial_cuda_attn_fwd, copies O (and lse when
+ *      non-NULL) back, synchronises.  Uses a per-thread cached device workspace. */
+int radial_cuda_attn_fwd_host(const void* q, const void* k, const void* v, void* o, float* lse,
+                              uint32_t heads, uint64_t n, uint32_t head_dim, float scale,
+                              const radial_layout* layout, void* stream);
+
+/* ---- backward (no reference exists; SPEC.md:8 scopes training out): gradients
+ *      of radial_cuda_attn_fwd over the same layout.  o / lse are the forward's
+ *      outputs; dq/dk/dv are bf16 [heads][n][head_dim].  workspace: device
+ *      scratch of radial_cuda_attn_bwd_workspace_size() bytes. */
+size_t radial_cuda_attn_bwd_workspace_size(uint32_t heads, uint64_t n, uint32_t head_dim);
+int radial_cuda_attn_bwd(const void* q, const void* k, const void* v, const void* o,
+                         const float* lse, const void* dout, void* dq, void* dk, void* dv,
+                         uint32_t heads, uint64_t n, uint32_t head_dim, float scale,
+                         const radial_layout* layout, void* workspace, void* stream);
+
+/* ---- accounting helpers: replace attention_flops / sparsity (block.hpp:123-148). */
+int radial_cuda_attention_flops(const radial_layout* layout, uint32_t head_dim, uint32_t heads,
+                                double* dense_flops, double* sparse_flops, double* reduction);
+double radial_cuda_sparsity(const radial_layout* layout);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RADIAL_CUDA_H */

@@ -82,6 +82,12 @@ def _load_ref():
     lib.ref_dense_attention.argtypes = [_u32, _u32, _u32, _f64p, _f64p, _f64p, _f64p]
     lib.ref_attention_flops.restype = _i32
     lib.ref_attention_flops.argtypes = [_u32, _u32, _u32, _i32, _u32, _u32] + [C.POINTER(_f64)] * 4
+    lib.ref_instance_create.restype = C.c_void_p
+    lib.ref_instance_create.argtypes = [_u32, _u32, _u32, _u64]
+    lib.ref_instance_free.restype = None
+    lib.ref_instance_free.argtypes = [C.c_void_p]
+    lib.ref_masked_attention_inst.restype = _i32
+    lib.ref_masked_attention_inst.argtypes = [C.c_void_p, _u32, _u32, _u64p, _u32p, C.c_void_p]
     return lib
 
 
@@ -257,3 +263,55 @@ def bf16_round(x: np.ndarray) -> np.ndarray:
     a = np.ascontiguousarray(x, np.float32).view(np.uint32).astype(np.uint64)
     a = (a + 0x7FFF + ((a >> 16) & 1)) & 0xFFFF0000
     return a.astype(np.uint32).view(np.float32)
+
+
+# --------------------------------------------------------------------------
+# CPU baseline: the reference's masked_attention on a bounded sample
+# --------------------------------------------------------------------------
+def sample_layout(row_ptr, col_idx, n, B, threads, per_thread=1):
+    """A layout for timing the reference on a bounded sample of the real workload:
+    `per_thread` query blocks inside each of the reference's static parallel_for chunks
+    (parallel.hpp:42-47, chunk = ceil(n/threads) tokens) keep their true KV lists; every
+    other block row keeps only its first kept block (so no row is empty).  Returns
+    (row_ptr, col_idx, kept_blocks_executed, sampled_blocks)."""
+    R = len(row_ptr) - 1
+    threads = max(1, min(threads, n))
+    chunk = -(-n // threads)
+    sampled = set()
+    for t in range(threads):
+        lo, hi = t * chunk, min(n, (t + 1) * chunk)
+        if lo >= hi:
+            break
+        for p in range(per_thread):
+            u = lo + (2 * p + 1) * (hi - lo) // (2 * per_thread)
+            sampled.add(min(u // B, R - 1))
+    lens = np.diff(row_ptr.astype(np.int64))
+    new_lens = np.where(np.isin(np.arange(R), sorted(sampled)), lens, np.minimum(lens, 1))
+    rp = np.concatenate([[0], np.cumsum(new_lens)]).astype(np.uint64)
+    ci = np.empty(int(rp[-1]), np.uint32)
+    for I in range(R):
+        a = int(row_ptr[I])
+        ci[int(rp[I]):int(rp[I + 1])] = col_idx[a:a + int(new_lens[I])]
+    return rp, ci, int(rp[-1]), sorted(sampled)
+
+
+class RefInstance:
+    """A persistent reference AttentionInstance (random_instance(f, s, d, seed))."""
+
+    def __init__(self, f, s, d, seed):
+        self.f, self.s, self.d = f, s, d
+        self.h = ref().ref_instance_create(f, s, d, seed)
+        if not self.h:
+            raise RuntimeError(ref().ref_last_error().decode())
+
+    def masked_attention(self, B, row_ptr, col_idx):
+        st = ref().ref_masked_attention_inst(self.h, B, len(row_ptr) - 1,
+                                             np.ascontiguousarray(row_ptr, np.uint64),
+                                             np.ascontiguousarray(col_idx, np.uint32), None)
+        if st != 0:
+            raise RuntimeError(ref().ref_last_error().decode())
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            ref().ref_instance_free(self.h)
+            self.h = None

@@ -169,3 +169,41 @@ int ref_attention_flops(uint32_t f, uint32_t s, uint32_t B, int sink, uint32_t h
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Persistent instances for timing the reference (bench.py's cpu baseline and
+// reference arm): the AttentionInstance is built once, outside the timed call.
+// ---------------------------------------------------------------------------
+extern "C" {
+
+void* ref_instance_create(uint32_t f, uint32_t s, uint32_t d, uint64_t seed) {
+    try {
+        return new radial::AttentionInstance(radial::random_instance(radial::GridShape(f, s), d, seed));
+    } catch (const std::exception& e) {
+        fail(e, -1);
+        return nullptr;
+    }
+}
+
+void ref_instance_free(void* inst) { delete static_cast<radial::AttentionInstance*>(inst); }
+
+// One radial::masked_attention(inst, layout) call (attention.hpp:229) on a
+// persistent instance; out may be NULL (result discarded).
+int ref_masked_attention_inst(void* inst_p, uint32_t B, uint32_t R, const uint64_t* row_ptr,
+                              const uint32_t* col_idx, double* out) {
+    try {
+        auto* inst = static_cast<radial::AttentionInstance*>(inst_p);
+        auto lay = make_layout(inst->shape.frames, inst->shape.tokens_per_frame, B, R, row_ptr, col_idx);
+        auto o = radial::masked_attention(*inst, lay);
+        if (out) std::memcpy(out, o.data.data(), o.data.size() * sizeof(double));
+        return 0;
+    } catch (const std::invalid_argument& e) {
+        return fail(e, 1);
+    } catch (const std::runtime_error& e) {
+        return fail(e, 2);
+    } catch (const std::exception& e) {
+        return fail(e, 3);
+    }
+}
+
+}  // extern "C"

@@ -1,0 +1,420 @@
+// attn_fwd.cu -- K2 (block-sparse radial forward) and K4 (dense comparator).
+//
+// Replaces radial::masked_attention(const AttentionInstance&, const BlockLayout&)
+// (reference attention.hpp:229-270) and radial::dense_attention
+// (attention.hpp:141-163): O = softmax(Q K^T * scale restricted to the kept
+// B x B blocks) V, computed for all heads in one launch.
+//
+// Work item = (head, chunk of 256 query rows).  A chunk is two 128-row Q
+// tiles that share every K/V tile load; the KV loop runs over the UNION of the
+// chunk's query-block lists (entry = J | mask << 28) and each tile skips the
+// blocks it does not keep, so FLOPs are exactly the kept blocks.
+//
+// Warp roles (384 threads, one CTA per SM):
+//   warp 0      TMA producer: Q tiles once, then K_j / V_j into 2-stage rings
+//   warp 1      MMA issuer (one thread): S_t = Q_t K_j^T (SS, both operands
+//               K-major in smem) and O_t += P_t V_j (TS: P from TMEM, V
+//               MN-major in smem), tcgen05.commit -> mbarriers
+//   warp 2      TMEM allocator (512 columns: S0 | S1 | O0 | O1)
+//   warps 4-7   softmax + epilogue for Q tile 0 (one thread per row = TMEM lane)
+//   warps 8-11  softmax + epilogue for Q tile 1
+// P (bf16) is written over its own S columns with tcgen05.st; the MMA issue
+// order (PV_t(j-1) before S_t(j)) makes that alias safe.  Online softmax in
+// the exp2 domain with lazy (threshold 8) rescaling of O in TMEM.
+#include <cmath>
+
+#include "radial_internal.h"
+#include "sm100.cuh"
+
+using namespace radial_sm100;
+
+namespace {
+
+constexpr int kThreads = 384;
+constexpr int kBQ = 128;        // query rows per tile
+constexpr int kStagesK = 2;
+constexpr int kStagesV = 2;
+constexpr float kRescaleThreshold = 8.0f;  // log2 units
+
+struct FwdParams {
+    __nv_bfloat16* o;
+    float* lse;
+    const uint64_t* uptr;
+    const uint32_t* uidx;
+    const uint32_t* order;
+    uint64_t n;
+    uint32_t heads, R, C;
+    float scale_log2;
+    int dense;
+};
+
+template <int D, int BK>
+struct FwdCfg {
+    static constexpr int G = 256 / BK;        // query blocks per chunk
+    static constexpr int GT = G / 2;          // query blocks per tile
+    static constexpr int kAtoms = D / 64;     // 64-column (128 B) swizzle atoms
+    static constexpr int kQAtomBytes = kBQ * 128;
+    static constexpr int kKVAtomBytes = BK * 128;
+    static constexpr int kQBytes = kBQ * D * 2;
+    static constexpr int kKVBytes = BK * D * 2;
+    static constexpr int kSmemQ = 0;
+    static constexpr int kSmemK = kSmemQ + 2 * kQBytes;
+    static constexpr int kSmemV = kSmemK + kStagesK * kKVBytes;
+    static constexpr int kSmemBar = kSmemV + kStagesV * kKVBytes;
+    static constexpr int kNumBars = 1 + 2 * kStagesK + 2 * kStagesV + 2 + 2 + 2;
+    static constexpr int kSmemBytes = kSmemBar + kNumBars * 8 + 16;
+    static constexpr int kSmemAlloc = kSmemBytes + 1024;  // slack for 1024 B alignment
+    // TMEM columns
+    static constexpr uint32_t kColS0 = 0, kColS1 = BK, kColO0 = 2 * BK, kColO1 = 2 * BK + D;
+    static constexpr uint32_t kTmemCols = (2 * BK + 2 * D) <= 256 ? 256 : 512;
+    static constexpr uint32_t kIdescS = idesc_bf16(128, BK, 0, 0);
+    static constexpr uint32_t kIdescO = idesc_bf16(128, D, 0, 1);
+};
+
+template <int D, int BK>
+__global__ void __launch_bounds__(kThreads, 1)
+    radial_attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q,
+                           const __grid_constant__ CUtensorMap tm_k,
+                           const __grid_constant__ CUtensorMap tm_v, const FwdParams p) {
+    using Cfg = FwdCfg<D, BK>;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                               ~static_cast<uintptr_t>(1023));
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Cfg::kSmemBar);
+    uint64_t* bar_q = bars;
+    uint64_t* bar_kfull = bars + 1;
+    uint64_t* bar_kempty = bar_kfull + kStagesK;
+    uint64_t* bar_vfull = bar_kempty + kStagesK;
+    uint64_t* bar_vempty = bar_vfull + kStagesV;
+    uint64_t* bar_sfull = bar_vempty + kStagesV;  // [2]
+    uint64_t* bar_pready = bar_sfull + 2;          // [2]
+    uint64_t* bar_ofull = bar_pready + 2;          // [2]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar_ofull + 2);
+
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+
+    // work item: all heads of the longest chunks first (LPT)
+    const uint32_t item = blockIdx.x;
+    const uint32_t head = item % p.heads;
+    const uint32_t chunk = p.order ? p.order[item / p.heads] : item / p.heads;
+    const uint64_t row0 = static_cast<uint64_t>(chunk) * 256;
+    uint64_t ebase = 0;
+    uint32_t L;
+    uint32_t dense_mask = 0;
+    if (p.dense) {
+        L = p.R;
+        for (int g = 0; g < Cfg::G; ++g)
+            if (chunk * Cfg::G + g < p.R) dense_mask |= 1u << g;
+    } else {
+        ebase = p.uptr[chunk];
+        L = static_cast<uint32_t>(p.uptr[chunk + 1] - ebase);
+    }
+    auto entry = [&](uint32_t j) -> uint32_t {
+        return p.dense ? (j | (dense_mask << 28)) : __ldg(p.uidx + ebase + j);
+    };
+
+    if (warp == 0 && lane == 0) {
+        mbar_init(bar_q, 1);
+        for (int s = 0; s < kStagesK; ++s) {
+            mbar_init(&bar_kfull[s], 1);
+            mbar_init(&bar_kempty[s], 1);
+        }
+        for (int s = 0; s < kStagesV; ++s) {
+            mbar_init(&bar_vfull[s], 1);
+            mbar_init(&bar_vempty[s], 1);
+        }
+        for (int t = 0; t < 2; ++t) {
+            mbar_init(&bar_sfull[t], 1);
+            mbar_init(&bar_pready[t], 128);
+            mbar_init(&bar_ofull[t], 1);
+        }
+        fence_barrier_init();
+        tma_prefetch_desc(&tm_q);
+        tma_prefetch_desc(&tm_k);
+        tma_prefetch_desc(&tm_v);
+    }
+    if (warp == 2) tmem_alloc(tmem_slot, Cfg::kTmemCols);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        // ------------------------------------------------------------ producer
+        if (lane == 0) {
+            const uint64_t pol_kv = l2_policy_evict_last();
+            mbar_arrive_expect_tx(bar_q, 2 * Cfg::kQBytes);
+            for (int t = 0; t < 2; ++t)
+                for (int a = 0; a < Cfg::kAtoms; ++a)
+                    tma_load_3d(smem + Cfg::kSmemQ + t * Cfg::kQBytes + a * Cfg::kQAtomBytes, &tm_q,
+                                bar_q, a * 64, static_cast<int32_t>(row0 + t * kBQ), head);
+            for (uint32_t j = 0; j < L; ++j) {
+                const int32_t J = static_cast<int32_t>(entry(j) & 0x0FFFFFFFu);
+                const int ks = j % kStagesK, vs = j % kStagesV;
+                mbar_wait(&bar_kempty[ks], ((j / kStagesK) & 1) ^ 1);
+                mbar_arrive_expect_tx(&bar_kfull[ks], Cfg::kKVBytes);
+                uint8_t* kd = smem + Cfg::kSmemK + ks * Cfg::kKVBytes;
+                for (int a = 0; a < Cfg::kAtoms; ++a)
+                    tma_load_3d_hint(kd + a * Cfg::kKVAtomBytes, &tm_k, &bar_kfull[ks], a * 64, J * BK,
+                                     head, pol_kv);
+                mbar_wait(&bar_vempty[vs], ((j / kStagesV) & 1) ^ 1);
+                mbar_arrive_expect_tx(&bar_vfull[vs], Cfg::kKVBytes);
+                uint8_t* vd = smem + Cfg::kSmemV + vs * Cfg::kKVBytes;
+                for (int a = 0; a < Cfg::kAtoms; ++a)
+                    tma_load_3d_hint(vd + a * Cfg::kKVAtomBytes, &tm_v, &bar_vfull[vs], a * 64, J * BK,
+                                     head, pol_kv);
+            }
+        }
+    } else if (warp == 1) {
+        // ------------------------------------------------------------ MMA issuer
+        if (lane == 0) {
+            mbar_wait(bar_q, 0);
+            tc_fence_after();
+            const uint32_t q_base = smem_u32(smem + Cfg::kSmemQ);
+            const uint32_t k_base = smem_u32(smem + Cfg::kSmemK);
+            const uint32_t v_base = smem_u32(smem + Cfg::kSmemV);
+            bool pend[2] = {false, false};
+            uint32_t acc[2] = {0, 0};
+            uint32_t pphase[2] = {0, 0};
+            for (uint32_t j = 0; j <= L; ++j) {
+                uint32_t tflag[2] = {0, 0};
+                const int ks = j % kStagesK;
+                if (j < L) {
+                    const uint32_t m = entry(j) >> 28;
+                    tflag[0] = m & ((1u << Cfg::GT) - 1);
+                    tflag[1] = (m >> Cfg::GT) & ((1u << Cfg::GT) - 1);
+                    mbar_wait(&bar_kfull[ks], (j / kStagesK) & 1);
+                }
+                if (j > 0 && (pend[0] || pend[1])) {
+                    mbar_wait(&bar_vfull[(j - 1) % kStagesV], ((j - 1) / kStagesV) & 1);
+                }
+                tc_fence_after();
+                for (int t = 0; t < 2; ++t) {
+                    if (pend[t]) {
+                        mbar_wait(&bar_pready[t], pphase[t]);
+                        pphase[t] ^= 1;
+                        tc_fence_after();
+                        const uint32_t vb = v_base + ((j - 1) % kStagesV) * Cfg::kKVBytes;
+                        const uint32_t p_col = t ? Cfg::kColS1 : Cfg::kColS0;
+                        const uint32_t o_col = t ? Cfg::kColO1 : Cfg::kColO0;
+#pragma unroll
+                        for (int kk = 0; kk < BK / 16; ++kk) {
+                            const uint64_t bdesc =
+                                sdesc_sw128(vb + kk * 16 * 128, Cfg::kKVAtomBytes, 1024);
+                            mma_ts(tmem + o_col, tmem + p_col + kk * 8, bdesc, Cfg::kIdescO,
+                                   (acc[t] | kk) ? 1u : 0u);
+                        }
+                        acc[t] = 1;
+                        pend[t] = false;
+                    }
+                    if (tflag[t]) {
+                        const uint32_t qb = q_base + t * Cfg::kQBytes;
+                        const uint32_t kb = k_base + ks * Cfg::kKVBytes;
+                        const uint32_t s_col = t ? Cfg::kColS1 : Cfg::kColS0;
+#pragma unroll
+                        for (int kk = 0; kk < D / 16; ++kk) {
+                            const uint32_t off_q = (kk >> 2) * Cfg::kQAtomBytes + (kk & 3) * 32;
+                            const uint32_t off_k = (kk >> 2) * Cfg::kKVAtomBytes + (kk & 3) * 32;
+                            mma_ss(tmem + s_col, sdesc_sw128(qb + off_q, 16, 1024),
+                                   sdesc_sw128(kb + off_k, 16, 1024), Cfg::kIdescS, kk ? 1u : 0u);
+                        }
+                        mma_commit(&bar_sfull[t]);
+                        pend[t] = true;
+                    }
+                }
+                if (j > 0) mma_commit(&bar_vempty[(j - 1) % kStagesV]);
+                if (j < L) mma_commit(&bar_kempty[ks]);
+            }
+            mma_commit(&bar_ofull[0]);
+            mma_commit(&bar_ofull[1]);
+        }
+    } else if (warp >= 4) {
+        // ------------------------------------------------------------ softmax
+        const int t = (warp - 4) >> 2;                 // Q tile
+        const int r = ((warp & 3) << 5) + lane;        // row in tile = TMEM lane
+        const uint32_t lane_addr = static_cast<uint32_t>((warp & 3) * 32) << 16;
+        const uint32_t s_addr = tmem + lane_addr + (t ? Cfg::kColS1 : Cfg::kColS0);
+        const uint32_t o_addr = tmem + lane_addr + (t ? Cfg::kColO1 : Cfg::kColO0);
+        const int my_bit = t * Cfg::GT + r / BK;
+        const uint64_t grow = row0 + t * kBQ + r;
+        const float sl2 = p.scale_log2;
+        float m = -INFINITY, l = 0.f;
+        uint32_t sphase = 0;
+        for (uint32_t j = 0; j < L; ++j) {
+            const uint32_t e = entry(j);
+            const uint32_t mask = e >> 28;
+            if (((mask >> (t * Cfg::GT)) & ((1u << Cfg::GT) - 1)) == 0) continue;
+            const uint32_t J = e & 0x0FFFFFFFu;
+            mbar_wait(&bar_sfull[t], sphase);
+            sphase ^= 1;
+            tc_fence_after();
+            float s[BK];
+#pragma unroll
+            for (int c = 0; c < BK; c += 32) {
+                uint32_t u[32];
+                tmem_ld32(s_addr + c, u);
+#pragma unroll
+                for (int x = 0; x < 32; ++x) s[c + x] = __uint_as_float(u[x]);
+            }
+            tmem_wait_ld();
+            const bool active = (mask >> my_bit) & 1;
+            const uint64_t kv0 = static_cast<uint64_t>(J) * BK;
+            const int valid = (kv0 + BK <= p.n) ? BK : static_cast<int>(p.n - kv0);
+            float mx = -INFINITY;
+#pragma unroll
+            for (int c = 0; c < BK; ++c) mx = fmaxf(mx, c < valid ? s[c] : -INFINITY);
+            const float m_cand = mx * sl2;
+            const bool need = active && (m == -INFINITY || m_cand > m + kRescaleThreshold);
+            const bool rescale = need && m != -INFINITY;
+            if (__any_sync(0xffffffffu, rescale)) {
+                const float alpha = rescale ? ex2(m - m_cand) : 1.f;
+#pragma unroll
+                for (int c = 0; c < D; c += 32) {
+                    uint32_t u[32];
+                    tmem_ld32(o_addr + c, u);
+                    tmem_wait_ld();
+#pragma unroll
+                    for (int x = 0; x < 32; ++x) u[x] = __float_as_uint(__uint_as_float(u[x]) * alpha);
+                    tmem_st32(o_addr + c, u);
+                }
+                if (rescale) l *= alpha;
+            }
+            if (need) m = m_cand;
+            uint32_t pk[BK / 2];
+            float rs = 0.f;
+            const float mb = active ? m : 0.f;
+#pragma unroll
+            for (int c = 0; c < BK; c += 2) {
+                float p0 = (active && c < valid) ? ex2(fmaf(s[c], sl2, -mb)) : 0.f;
+                float p1 = (active && c + 1 < valid) ? ex2(fmaf(s[c + 1], sl2, -mb)) : 0.f;
+                rs += p0 + p1;
+                pk[c / 2] = pack_bf16(p0, p1);
+            }
+            l += rs;
+#pragma unroll
+            for (int c = 0; c < BK / 2; c += 16) tmem_st16(s_addr + c, pk + c);
+            tmem_wait_st();
+            tc_fence_before();
+            mbar_arrive(&bar_pready[t]);
+        }
+        // ------------------------------------------------------------ epilogue
+        mbar_wait(&bar_ofull[t], 0);
+        tc_fence_after();
+        const float inv = l > 0.f ? 1.f / l : 0.f;
+        __nv_bfloat16* orow = p.o + (static_cast<uint64_t>(head) * p.n + grow) * D;
+#pragma unroll
+        for (int c = 0; c < D; c += 32) {
+            uint32_t u[32];
+            tmem_ld32(o_addr + c, u);
+            tmem_wait_ld();
+            uint32_t w[16];
+#pragma unroll
+            for (int x = 0; x < 16; ++x)
+                w[x] = pack_bf16(__uint_as_float(u[2 * x]) * inv, __uint_as_float(u[2 * x + 1]) * inv);
+            if (grow < p.n) {
+                uint4* dst = reinterpret_cast<uint4*>(orow + c);
+#pragma unroll
+                for (int x = 0; x < 4; ++x) dst[x] = make_uint4(w[4 * x], w[4 * x + 1], w[4 * x + 2], w[4 * x + 3]);
+            }
+        }
+        if (p.lse && grow < p.n)
+            p.lse[static_cast<uint64_t>(head) * p.n + grow] =
+                l > 0.f ? (m + __log2f(l)) * 0.69314718055994531f : -INFINITY;
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 2) {
+        tc_fence_after();
+        tmem_dealloc(tmem, Cfg::kTmemCols);
+    }
+}
+
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+    static EncodeTiledFn fn = [] {
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            f = nullptr;
+        return reinterpret_cast<EncodeTiledFn>(f);
+    }();
+    return fn;
+}
+
+}  // namespace
+
+namespace radial_detail {
+
+// bf16 [heads][n][D] tensor map with a (64 x rows x 1) box, 128 B swizzle,
+// zero fill out of bounds (tail rows / keys beyond n).
+int make_tmap_bf16_3d(CUtensorMap* m, const void* base, uint64_t n, uint32_t D, uint32_t heads,
+                      uint32_t box_rows) {
+    EncodeTiledFn fn = encode_fn();
+    if (!fn) return fail(RADIAL_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    if (reinterpret_cast<uintptr_t>(base) % 16 != 0)
+        return fail(RADIAL_ERR_INVALID, "tensor base must be 16-byte aligned");
+    cuuint64_t dims[3] = {D, n, heads};
+    cuuint64_t strides[2] = {static_cast<cuuint64_t>(D) * 2, static_cast<cuuint64_t>(D) * 2 * n};
+    cuuint32_t box[3] = {64, box_rows, 1};
+    cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides,
+                    box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(RADIAL_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(r));
+    return RADIAL_OK;
+}
+
+template <int D, int BK>
+int launch_fwd_t(const void* q, const void* k, const void* v, void* o, float* lse,
+                 uint32_t heads, uint64_t n, float scale, const radial_layout* L, uint32_t R,
+                 cudaStream_t st) {
+    using Cfg = FwdCfg<D, BK>;
+    CUtensorMap tq, tk, tv;
+    int rc;
+    if ((rc = make_tmap_bf16_3d(&tq, q, n, D, heads, kBQ))) return rc;
+    if ((rc = make_tmap_bf16_3d(&tk, k, n, D, heads, BK))) return rc;
+    if ((rc = make_tmap_bf16_3d(&tv, v, n, D, heads, BK))) return rc;
+    FwdParams p{};
+    p.o = static_cast<__nv_bfloat16*>(o);
+    p.lse = lse;
+    p.n = n;
+    p.heads = heads;
+    p.R = R;
+    p.C = (R + Cfg::G - 1) / Cfg::G;
+    p.scale_log2 = scale * 1.4426950408889634f;
+    p.dense = L == nullptr;
+    if (L) {
+        p.uptr = L->uptr;
+        p.uidx = L->uidx;
+        p.order = L->uorder;
+    }
+    auto kern = radial_attn_fwd_kernel<D, BK>;
+    RADIAL_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmemAlloc));
+    const uint64_t items = static_cast<uint64_t>(p.C) * heads;
+    if (items == 0) return RADIAL_OK;
+    if (items > 0x7fffffffull) return fail(RADIAL_ERR_INVALID, "too many work items");
+    kern<<<static_cast<unsigned>(items), kThreads, Cfg::kSmemAlloc, st>>>(tq, tk, tv, p);
+    RADIAL_CUDA_TRY(cudaGetLastError());
+    return RADIAL_OK;
+}
+
+int launch_fwd(const void* q, const void* k, const void* v, void* o, float* lse, uint32_t heads,
+               uint64_t n, uint32_t D, uint32_t BK, float scale, const radial_layout* L,
+               cudaStream_t st) {
+    const uint64_t R64 = (n + BK - 1) / BK;
+    if (R64 >= (1ull << 28)) return fail(RADIAL_ERR_INVALID, "block grid too large for the kernel");
+    const uint32_t R = static_cast<uint32_t>(R64);
+    if (D == 128 && BK == 128) return launch_fwd_t<128, 128>(q, k, v, o, lse, heads, n, scale, L, R, st);
+    if (D == 128 && BK == 64) return launch_fwd_t<128, 64>(q, k, v, o, lse, heads, n, scale, L, R, st);
+    if (D == 64 && BK == 128) return launch_fwd_t<64, 128>(q, k, v, o, lse, heads, n, scale, L, R, st);
+    if (D == 64 && BK == 64) return launch_fwd_t<64, 64>(q, k, v, o, lse, heads, n, scale, L, R, st);
+    return fail(RADIAL_ERR_INVALID, "masked_attention: head_dim must be 64 or 128 and block_size 64 or 128");
+}
+
+}  // namespace radial_detail

@@ -1,0 +1,114 @@
+// debug_mma.cu -- single-tile self-test of the tcgen05 building blocks used by
+// the attention kernels (TMA SWIZZLE_128B loads, SS MMA with K-major operands,
+// TMEM A-operand TS MMA with an MN-major B operand, tcgen05.ld/st).
+// Exposed as radial_cuda_debug_tile() for the GPU test-suite only.
+#include "radial_internal.h"
+#include "sm100.cuh"
+
+using namespace radial_sm100;
+
+namespace radial_detail {
+int make_tmap_bf16_3d(CUtensorMap* m, const void* base, uint64_t n, uint32_t D, uint32_t heads,
+                      uint32_t box_rows);
+}
+
+namespace {
+
+// S = Q K^T (128x128x128), then O = P V with P supplied (bf16 128x128).
+__global__ void __launch_bounds__(192, 1)
+    debug_tile_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
+                      const __grid_constant__ CUtensorMap tm_v, const __nv_bfloat16* __restrict__ p_in,
+                      float* __restrict__ s_out, float* __restrict__ o_out) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                               ~static_cast<uintptr_t>(1023));
+    constexpr int kT = 128 * 128 * 2;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 3 * kT);
+    uint32_t* slot = reinterpret_cast<uint32_t*>(bars + 4);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        mbar_init(&bars[0], 1);    // tma
+        mbar_init(&bars[1], 1);    // S done
+        mbar_init(&bars[2], 128);  // P written
+        mbar_init(&bars[3], 1);    // O done
+        fence_barrier_init();
+    }
+    if (warp == 1) tmem_alloc(slot, 512);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *slot;
+    constexpr uint32_t idS = idesc_bf16(128, 128, 0, 0);
+    constexpr uint32_t idO = idesc_bf16(128, 128, 0, 1);
+    if (warp == 0 && lane == 0) {
+        mbar_arrive_expect_tx(&bars[0], 3 * kT);
+        for (int a = 0; a < 2; ++a) {
+            tma_load_3d(smem + a * 16384, &tm_q, &bars[0], a * 64, 0, 0);
+            tma_load_3d(smem + kT + a * 16384, &tm_k, &bars[0], a * 64, 0, 0);
+            tma_load_3d(smem + 2 * kT + a * 16384, &tm_v, &bars[0], a * 64, 0, 0);
+        }
+        mbar_wait(&bars[0], 0);
+        tc_fence_after();
+        const uint32_t qb = smem_u32(smem), kb = smem_u32(smem + kT), vb = smem_u32(smem + 2 * kT);
+        for (int kk = 0; kk < 8; ++kk) {
+            const uint32_t off = (kk >> 2) * 16384 + (kk & 3) * 32;
+            mma_ss(tmem, sdesc_sw128(qb + off, 16, 1024), sdesc_sw128(kb + off, 16, 1024), idS, kk ? 1u : 0u);
+        }
+        mma_commit(&bars[1]);
+        mbar_wait(&bars[2], 0);
+        tc_fence_after();
+        for (int kk = 0; kk < 8; ++kk)
+            mma_ts(tmem + 256, tmem + kk * 8, sdesc_sw128(vb + kk * 2048, 16384, 1024), idO, kk ? 1u : 0u);
+        mma_commit(&bars[3]);
+    } else if (warp >= 2) {
+        const int r = ((warp & 3) << 5) + lane;
+        const uint32_t la = static_cast<uint32_t>((warp & 3) * 32) << 16;
+        mbar_wait(&bars[1], 0);
+        tc_fence_after();
+        for (int c = 0; c < 128; c += 32) {
+            uint32_t u[32];
+            tmem_ld32(tmem + la + c, u);
+            tmem_wait_ld();
+            for (int x = 0; x < 32; ++x) s_out[r * 128 + c + x] = __uint_as_float(u[x]);
+        }
+        uint32_t pk[64];
+        for (int x = 0; x < 64; ++x)
+            pk[x] = pack_bf16(__bfloat162float(p_in[r * 128 + 2 * x]), __bfloat162float(p_in[r * 128 + 2 * x + 1]));
+        for (int c = 0; c < 64; c += 16) tmem_st16(tmem + la + c, pk + c);
+        tmem_wait_st();
+        tc_fence_before();
+        mbar_arrive(&bars[2]);
+        mbar_wait(&bars[3], 0);
+        tc_fence_after();
+        for (int c = 0; c < 128; c += 32) {
+            uint32_t u[32];
+            tmem_ld32(tmem + la + 256 + c, u);
+            tmem_wait_ld();
+            for (int x = 0; x < 32; ++x) o_out[r * 128 + c + x] = __uint_as_float(u[x]);
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        tmem_dealloc(tmem, 512);
+    }
+}
+
+}  // namespace
+
+extern "C" int radial_cuda_debug_tile(const void* q, const void* k, const void* v, const void* p,
+                                      float* s_out, float* o_out, void* stream) {
+    using namespace radial_detail;
+    CUtensorMap tq, tk, tv;
+    int rc;
+    if ((rc = make_tmap_bf16_3d(&tq, q, 128, 128, 1, 128))) return rc;
+    if ((rc = make_tmap_bf16_3d(&tk, k, 128, 128, 1, 128))) return rc;
+    if ((rc = make_tmap_bf16_3d(&tv, v, 128, 128, 1, 128))) return rc;
+    const int smem = 3 * 128 * 128 * 2 + 64 + 1024;
+    RADIAL_CUDA_TRY(cudaFuncSetAttribute(debug_tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    debug_tile_kernel<<<1, 192, smem, static_cast<cudaStream_t>(stream)>>>(
+        tq, tk, tv, static_cast<const __nv_bfloat16*>(p), s_out, o_out);
+    RADIAL_CUDA_TRY(cudaGetLastError());
+    return RADIAL_OK;
+}

@@ -1,0 +1,357 @@
+// mask_build.cu -- K1: on-device radial block-layout builder.
+//
+// Replaces radial::blockify (reference block.hpp:59-120).  The reference
+// paints, per query block row, every kept key interval of every key frame
+// (kept_span, mask.hpp:105-154) into a hit bitmap.  Here each (I, J) block
+// pair is decided independently by a closed-form predicate: (I, J) is kept
+// iff some query frame i overlapping block I and key frame j overlapping
+// block J have kept_span(i, [k_lo,k_hi], j) intersecting J's positions in
+// frame j.  That is exactly the set of J the reference paints, so the CSR is
+// bit-identical (gated by sha256 of the .ramk bytes in tests/).
+//
+// One CTA per output row sweeps the columns 256 at a time; rows are
+// compacted with warp ballots so col_idx comes out strictly increasing
+// without a sort.  Three list families are built with the same machinery:
+//   CSR   rows = query blocks, cols = KV blocks     (BlockLayout)
+//   CSC   rows = KV blocks,    cols = query blocks  (backward dK/dV)
+//   chunk unions: rows = 256-token chunks, value = J | mask << 28
+//         (the forward / backward work lists).
+#include <algorithm>
+#include <numeric>
+#include <vector>
+
+#include "radial_internal.h"
+
+namespace {
+
+constexpr int kThreads = 256;
+
+struct MaskParams {
+    uint32_t f, s, B;
+    uint64_t n;
+    int kind, sink;
+    uint32_t tw, sw;
+};
+
+// mask.hpp:105-154 kept_span for every frame-structured kind.
+__device__ __forceinline__ bool kept_span(const MaskParams& p, uint32_t i, uint32_t k_lo,
+                                          uint32_t k_hi, uint32_t j, uint32_t& lo, uint32_t& hi) {
+    const uint32_t s = p.s;
+    const uint64_t d = i < j ? j - i : i - j;
+    auto band = [&](uint32_t sigma) {
+        lo = k_lo > sigma ? k_lo - sigma : 0;
+        uint64_t h = static_cast<uint64_t>(k_hi) + sigma;
+        hi = h >= s ? s - 1 : static_cast<uint32_t>(h);
+        return true;
+    };
+    if (p.sink && j == 0) {
+        lo = 0;
+        hi = s - 1;
+        return true;
+    }
+    switch (p.kind) {
+        case RADIAL_KIND_DENSE:
+            lo = 0;
+            hi = s - 1;
+            return true;
+        case RADIAL_KIND_RADIAL: {
+            const uint32_t e = d <= 1 ? 0u : 63u - __clzll(d);
+            const uint64_t pw = 1ull << e;
+            if (pw <= s) return band(static_cast<uint32_t>(s / pw) - 1);
+            const uint64_t period = (pw + s - 1) / s;
+            if (d % period == 0) {
+                lo = k_lo;
+                hi = k_hi;
+                return true;
+            }
+            return false;
+        }
+        case RADIAL_KIND_SPATIAL:
+            if (d <= p.tw) {
+                lo = 0;
+                hi = s - 1;
+                return true;
+            }
+            return false;
+        case RADIAL_KIND_TEMPORAL:
+            return band(min(p.sw, s - 1));
+        case RADIAL_KIND_STA:
+            if (d <= p.tw) return band(min(p.sw, s - 1));
+            return false;
+        case RADIAL_KIND_HARMONIC: {
+            const uint64_t dist = d < 1 ? 1 : d;
+            const uint64_t width = s / dist;
+            if (width >= 1) return band(static_cast<uint32_t>(width) - 1);
+            const uint64_t period = (dist + s - 1) / s;
+            if (d % period == 0) {
+                lo = k_lo;
+                hi = k_hi;
+                return true;
+            }
+            return false;
+        }
+        default:
+            return false;
+    }
+}
+
+// Block (I, J) kept?  Frame-structured kinds: exact per-pair restatement of
+// the painting in block.hpp:81-97.  Power: block-level rule block.hpp:71-80.
+struct BlockKeep {
+    MaskParams p;
+    __device__ __forceinline__ uint32_t operator()(uint32_t I, uint32_t J) const {
+        const uint64_t B = p.B, s = p.s;
+        if (p.kind == RADIAL_KIND_POWER) {
+            const uint32_t t = I > J ? I - J : J - I;
+            if ((t & (t - 1)) == 0) return 1;  // t == 0 or a power of two
+            return (p.sink && J <= (s - 1) / B) ? 1 : 0;
+        }
+        const uint64_t u0 = static_cast<uint64_t>(I) * B;
+        const uint64_t u1 = min(p.n, u0 + B) - 1;
+        const uint64_t v0 = static_cast<uint64_t>(J) * B;
+        const uint64_t v1 = min(p.n, v0 + B) - 1;
+        for (uint64_t i = u0 / s; i * s <= u1; ++i) {
+            const uint32_t k_lo = static_cast<uint32_t>(max(u0, i * s) - i * s);
+            const uint32_t k_hi = static_cast<uint32_t>(min(u1, i * s + s - 1) - i * s);
+            for (uint64_t j = v0 / s; j * s <= v1; ++j) {
+                const uint32_t l_lo = static_cast<uint32_t>(max(v0, j * s) - j * s);
+                const uint32_t l_hi = static_cast<uint32_t>(min(v1, j * s + s - 1) - j * s);
+                uint32_t lo, hi;
+                if (kept_span(p, static_cast<uint32_t>(i), k_lo, k_hi, static_cast<uint32_t>(j), lo,
+                              hi) &&
+                    lo <= l_hi && hi >= l_lo)
+                    return 1;
+            }
+        }
+        return 0;
+    }
+};
+
+__device__ __forceinline__ bool csr_member(const uint64_t* __restrict__ ptr,
+                                           const uint32_t* __restrict__ idx, uint32_t row,
+                                           uint32_t col) {
+    uint64_t lo = ptr[row], hi = ptr[row + 1];
+    while (lo < hi) {
+        const uint64_t mid = (lo + hi) >> 1;
+        const uint32_t v = idx[mid];
+        if (v == col) return true;
+        if (v < col)
+            lo = mid + 1;
+        else
+            hi = mid;
+    }
+    return false;
+}
+
+// Transpose: row = KV block J, col = query block I, kept iff J in CSR row I.
+struct CsrTranspose {
+    const uint64_t* ptr;
+    const uint32_t* idx;
+    __device__ __forceinline__ uint32_t operator()(uint32_t J, uint32_t I) const {
+        return csr_member(ptr, idx, I, J) ? 1u : 0u;
+    }
+};
+
+// Chunk union: row = chunk c (G consecutive rows of the source lists),
+// value = bit g set iff source row c*G+g contains col.
+struct ChunkUnion {
+    const uint64_t* ptr;
+    const uint32_t* idx;
+    uint32_t R, G;
+    __device__ __forceinline__ uint32_t operator()(uint32_t c, uint32_t col) const {
+        uint32_t m = 0;
+        for (uint32_t g = 0; g < G; ++g) {
+            const uint32_t r = c * G + g;
+            if (r < R && csr_member(ptr, idx, r, col)) m |= 1u << g;
+        }
+        return m;
+    }
+};
+
+template <class F>
+__global__ void __launch_bounds__(kThreads) list_count(F pred, uint32_t cols,
+                                                      uint32_t* __restrict__ counts) {
+    const uint32_t row = blockIdx.x;
+    uint32_t c = 0;
+    for (uint32_t base = 0; base < cols; base += kThreads) {
+        const uint32_t col = base + threadIdx.x;
+        const bool keep = col < cols && pred(row, col) != 0;
+        c += __popc(__ballot_sync(0xffffffffu, keep));
+    }
+    __shared__ uint32_t warp_sum[kThreads / 32];
+    if ((threadIdx.x & 31) == 0) warp_sum[threadIdx.x >> 5] = c;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t t = 0;
+        for (int w = 0; w < kThreads / 32; ++w) t += warp_sum[w];
+        counts[row] = t;
+    }
+}
+
+template <class F>
+__global__ void __launch_bounds__(kThreads) list_fill(F pred, uint32_t cols,
+                                                     const uint64_t* __restrict__ ptr,
+                                                     uint32_t* __restrict__ out, int with_mask) {
+    const uint32_t row = blockIdx.x;
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    __shared__ uint32_t warp_cnt[kThreads / 32];
+    uint64_t pos = ptr[row];
+    for (uint32_t base = 0; base < cols; base += kThreads) {
+        const uint32_t col = base + threadIdx.x;
+        const uint32_t v = col < cols ? pred(row, col) : 0u;
+        const uint32_t bal = __ballot_sync(0xffffffffu, v != 0);
+        if (lane == 0) warp_cnt[warp] = __popc(bal);
+        __syncthreads();
+        uint32_t before = 0, total = 0;
+        for (uint32_t w = 0; w < kThreads / 32; ++w) {
+            const uint32_t cw = warp_cnt[w];
+            before += w < warp ? cw : 0;
+            total += cw;
+        }
+        if (v) {
+            const uint32_t rank = before + __popc(bal & ((1u << lane) - 1u));
+            out[pos + rank] = with_mask ? (col | (v << 28)) : col;
+        }
+        pos += total;
+        __syncthreads();
+    }
+}
+
+struct ScanStats {
+    unsigned long long nnz;
+    long long first_empty;
+    uint32_t max_len, min_len;
+};
+
+// Exclusive scan of u32 counts into u64 pointers, plus row-length stats.
+__global__ void __launch_bounds__(1024) scan_rows(const uint32_t* __restrict__ counts,
+                                                  uint32_t rows, uint64_t* __restrict__ ptr,
+                                                  ScanStats* stats) {
+    __shared__ uint64_t warp_tot[32];
+    __shared__ uint64_t carry;
+    __shared__ long long first_empty;
+    __shared__ uint32_t mx, mn;
+    if (threadIdx.x == 0) {
+        carry = 0;
+        first_empty = -1;
+        mx = 0;
+        mn = 0xffffffffu;
+        ptr[0] = 0;
+    }
+    __syncthreads();
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint32_t local_max = 0, local_min = 0xffffffffu;
+    long long local_empty = -1;
+    for (uint32_t base = 0; base < rows; base += 1024) {
+        const uint32_t r = base + threadIdx.x;
+        const uint64_t c = r < rows ? counts[r] : 0;
+        if (r < rows) {
+            local_max = max(local_max, static_cast<uint32_t>(c));
+            local_min = min(local_min, static_cast<uint32_t>(c));
+            if (c == 0 && local_empty < 0) local_empty = r;
+        }
+        uint64_t x = c;  // inclusive warp scan
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint64_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        if (lane == 31) warp_tot[warp] = x;
+        __syncthreads();
+        uint64_t before = 0, total = 0;
+        for (uint32_t w = 0; w < 32; ++w) {
+            before += w < warp ? warp_tot[w] : 0;
+            total += warp_tot[w];
+        }
+        if (r < rows) ptr[r + 1] = carry + before + x;
+        __syncthreads();
+        if (threadIdx.x == 0) carry += total;
+        __syncthreads();
+    }
+    atomicMax(&mx, local_max);
+    atomicMin(&mn, local_min);
+    if (local_empty >= 0) atomicMin(reinterpret_cast<unsigned long long*>(&first_empty),
+                                    static_cast<unsigned long long>(local_empty));
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        stats->nnz = carry;
+        stats->first_empty = first_empty;
+        stats->max_len = mx;
+        stats->min_len = rows ? mn : 0;
+    }
+}
+
+// Builds ptr/idx lists for `rows` rows over `cols` columns with predicate F.
+template <class F>
+int build_lists(F pred, uint32_t rows, uint32_t cols, int with_mask, cudaStream_t st,
+                uint64_t** ptr_out, uint32_t** idx_out, ScanStats* host_stats) {
+    uint32_t* counts = nullptr;
+    ScanStats* dstats = nullptr;
+    RADIAL_CUDA_TRY(cudaMallocAsync(&counts, sizeof(uint32_t) * std::max<uint32_t>(rows, 1), st));
+    RADIAL_CUDA_TRY(cudaMallocAsync(&dstats, sizeof(ScanStats), st));
+    RADIAL_CUDA_TRY(cudaMalloc(ptr_out, sizeof(uint64_t) * (static_cast<size_t>(rows) + 1)));
+    if (rows) list_count<F><<<rows, kThreads, 0, st>>>(pred, cols, counts);
+    scan_rows<<<1, 1024, 0, st>>>(counts, rows, *ptr_out, dstats);
+    RADIAL_CUDA_TRY(cudaGetLastError());
+    RADIAL_CUDA_TRY(cudaMemcpyAsync(host_stats, dstats, sizeof(ScanStats), cudaMemcpyDeviceToHost, st));
+    RADIAL_CUDA_TRY(cudaStreamSynchronize(st));
+    RADIAL_CUDA_TRY(cudaMalloc(idx_out, sizeof(uint32_t) * std::max<uint64_t>(host_stats->nnz, 1)));
+    if (rows) list_fill<F><<<rows, kThreads, 0, st>>>(pred, cols, *ptr_out, *idx_out, with_mask);
+    RADIAL_CUDA_TRY(cudaGetLastError());
+    RADIAL_CUDA_TRY(cudaFreeAsync(counts, st));
+    RADIAL_CUDA_TRY(cudaFreeAsync(dstats, st));
+    return RADIAL_OK;
+}
+
+// Longest-processing-time-first order of chunks (by work-list length).
+int lpt_order(const uint64_t* dptr, uint32_t C, cudaStream_t st, uint32_t** order_out) {
+    std::vector<uint64_t> h(C + 1);
+    RADIAL_CUDA_TRY(cudaMemcpyAsync(h.data(), dptr, sizeof(uint64_t) * (C + 1), cudaMemcpyDeviceToHost, st));
+    RADIAL_CUDA_TRY(cudaStreamSynchronize(st));
+    std::vector<uint32_t> ord(C);
+    std::iota(ord.begin(), ord.end(), 0u);
+    std::stable_sort(ord.begin(), ord.end(), [&](uint32_t a, uint32_t b) {
+        return (h[a + 1] - h[a]) > (h[b + 1] - h[b]);
+    });
+    RADIAL_CUDA_TRY(cudaMalloc(order_out, sizeof(uint32_t) * std::max<uint32_t>(C, 1)));
+    RADIAL_CUDA_TRY(cudaMemcpyAsync(*order_out, ord.data(), sizeof(uint32_t) * C, cudaMemcpyHostToDevice, st));
+    RADIAL_CUDA_TRY(cudaStreamSynchronize(st));
+    return RADIAL_OK;
+}
+
+}  // namespace
+
+namespace radial_detail {
+
+int build_layout_device(radial_layout* L, cudaStream_t st) {
+    MaskParams p{L->f, L->s, L->B, static_cast<uint64_t>(L->f) * L->s, L->kind, L->sink, L->tw, L->sw};
+    ScanStats hs{};
+    int rc = build_lists(BlockKeep{p}, L->R, L->R, 0, st, &L->row_ptr, &L->col_idx, &hs);
+    if (rc) return rc;
+    L->nnz = hs.nnz;
+    L->first_empty_row = hs.first_empty;
+    L->max_row_len = hs.max_len;
+    L->min_row_len = hs.min_len;
+    return RADIAL_OK;
+}
+
+int build_worklists(radial_layout* L, cudaStream_t st) {
+    ScanStats hs{};
+    int rc = build_lists(CsrTranspose{L->row_ptr, L->col_idx}, L->R, L->R, 0, st, &L->col_ptr,
+                         &L->row_idx, &hs);
+    if (rc) return rc;
+    if (hs.nnz != L->nnz) return fail(RADIAL_ERR_INVALID, "layout transpose size mismatch");
+    if (L->B != 64 && L->B != 128) return RADIAL_OK;  // attention kernels not instantiated
+    L->G = 256 / L->B;
+    L->C = (L->R + L->G - 1) / L->G;
+    rc = build_lists(ChunkUnion{L->row_ptr, L->col_idx, L->R, L->G}, L->C, L->R, 1, st, &L->uptr,
+                     &L->uidx, &hs);
+    if (rc) return rc;
+    rc = lpt_order(L->uptr, L->C, st, &L->uorder);
+    if (rc) return rc;
+    rc = build_lists(ChunkUnion{L->col_ptr, L->row_idx, L->R, L->G}, L->C, L->R, 1, st, &L->tptr,
+                     &L->tidx, &hs);
+    if (rc) return rc;
+    return lpt_order(L->tptr, L->C, st, &L->torder);
+}
+
+}  // namespace radial_detail

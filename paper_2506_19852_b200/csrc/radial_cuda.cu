@@ -1,0 +1,336 @@
+// radial_cuda.cu -- the C-ABI (include/radial_cuda.h): layout handles,
+// argument validation with the reference's error semantics, launches.
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "radial_internal.h"
+
+namespace radial_detail {
+
+thread_local std::string g_last_error;
+
+void set_error(const std::string& msg) { g_last_error = msg; }
+int fail(int code, const std::string& msg) {
+    g_last_error = msg;
+    return code;
+}
+int cuda_fail(cudaError_t e, const char* where) {
+    g_last_error = std::string("CUDA error ") + cudaGetErrorName(e) + " (" + cudaGetErrorString(e) +
+                   ") at " + where;
+    return e == cudaErrorMemoryAllocation ? RADIAL_ERR_OOM : RADIAL_ERR_CUDA;
+}
+
+int launch_fwd(const void* q, const void* k, const void* v, void* o, float* lse, uint32_t heads,
+               uint64_t n, uint32_t D, uint32_t BK, float scale, const radial_layout* L,
+               cudaStream_t st);
+int launch_bwd(const void* q, const void* k, const void* v, const void* o, const float* lse,
+               const void* dout, void* dq, void* dk, void* dv, uint32_t heads, uint64_t n,
+               uint32_t D, float scale, const radial_layout* L, void* workspace, cudaStream_t st);
+size_t bwd_workspace_bytes(uint32_t heads, uint64_t n, uint32_t D);
+
+}  // namespace radial_detail
+
+using namespace radial_detail;
+
+namespace {
+
+void free_layout(radial_layout* L) {
+    if (!L) return;
+    void* ptrs[] = {L->row_ptr, L->col_idx, L->col_ptr, L->row_idx, L->uptr,
+                    L->uidx,    L->uorder,  L->tptr,    L->tidx,    L->torder};
+    for (void* p : ptrs)
+        if (p) cudaFree(p);
+    delete L;
+}
+
+int check_shape(uint32_t f, uint32_t s, uint32_t B) {
+    if (f < 1 || s < 1)
+        return fail(RADIAL_ERR_INVALID, "GridShape: frames and tokens_per_frame must be >= 1");
+    if (static_cast<uint64_t>(f) * s > (1ull << 32))
+        return fail(RADIAL_ERR_INVALID, "GridShape: total tokens exceeds 2^32");
+    if (B < 1) return fail(RADIAL_ERR_INVALID, "blockify: block_size must be >= 1");
+    const uint64_t rows = (static_cast<uint64_t>(f) * s + B - 1) / B;
+    if (rows > 0xffffffffull) return fail(RADIAL_ERR_LENGTH, "block grid exceeds 2^32 rows");
+    return RADIAL_OK;
+}
+
+int check_pattern(int kind, uint32_t tw, uint32_t sw, bool has_tw, bool has_sw) {
+    if (kind < 0 || kind > RADIAL_KIND_HARMONIC) return fail(RADIAL_ERR_INVALID, "unknown pattern kind");
+    (void)tw;
+    (void)sw;
+    (void)has_tw;
+    (void)has_sw;
+    return RADIAL_OK;
+}
+
+int check_attn(const void* q, const void* k, const void* v, const void* o, uint32_t heads,
+               uint64_t n, uint32_t D) {
+    if (!q || !k || !v || !o) return fail(RADIAL_ERR_INVALID, "masked_attention: null tensor");
+    if (heads < 1 || n < 1) return fail(RADIAL_ERR_INVALID, "masked_attention: heads and n must be >= 1");
+    if (D != 64 && D != 128)
+        return fail(RADIAL_ERR_INVALID, "masked_attention: head_dim must be 64 or 128 on the device path");
+    return RADIAL_OK;
+}
+
+int check_layout_for_attn(const radial_layout* L, uint64_t n) {
+    if (!L) return fail(RADIAL_ERR_INVALID, "masked_attention: null layout");
+    if (static_cast<uint64_t>(L->f) * L->s != n)
+        return fail(RADIAL_ERR_INVALID, "masked_attention: layout shape mismatch");
+    if (L->B != 64 && L->B != 128)
+        return fail(RADIAL_ERR_INVALID, "masked_attention: block_size must be 64 or 128 on the device path");
+    if (L->first_empty_row >= 0)
+        return fail(RADIAL_ERR_EMPTY_ROW,
+                    "masked_attention: query row " +
+                        std::to_string(static_cast<uint64_t>(L->first_empty_row) * L->B) +
+                        " keeps no keys");
+    return RADIAL_OK;
+}
+
+float resolve_scale(float scale, uint32_t D) {
+    return scale > 0.f ? scale : static_cast<float>(1.0 / std::sqrt(static_cast<double>(D)));
+}
+
+}  // namespace
+
+extern "C" {
+
+int radial_cuda_abi_version(void) { return RADIAL_CUDA_ABI_VERSION; }
+const char* radial_cuda_last_error(void) { return g_last_error.c_str(); }
+
+int radial_cuda_mask_build(uint32_t frames, uint32_t tokens_per_frame, uint32_t block_size, int kind,
+                           int sink, uint32_t temporal_window, uint32_t spatial_window, void* stream,
+                           radial_layout** out) {
+    if (!out) return fail(RADIAL_ERR_INVALID, "null output handle");
+    *out = nullptr;
+    int rc = check_shape(frames, tokens_per_frame, block_size);
+    if (rc) return rc;
+    if ((rc = check_pattern(kind, temporal_window, spatial_window, true, true))) return rc;
+    auto* L = new radial_layout();
+    RADIAL_CUDA_TRY(cudaGetDevice(&L->device));
+    L->f = frames;
+    L->s = tokens_per_frame;
+    L->B = block_size;
+    L->R = static_cast<uint32_t>((static_cast<uint64_t>(frames) * tokens_per_frame + block_size - 1) / block_size);
+    L->kind = static_cast<uint8_t>(kind);
+    L->sink = sink ? 1 : 0;
+    L->tw = temporal_window;
+    L->sw = spatial_window;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if ((rc = build_layout_device(L, st)) || (rc = build_worklists(L, st))) {
+        free_layout(L);
+        return rc;
+    }
+    *out = L;
+    return RADIAL_OK;
+}
+
+int radial_cuda_layout_from_csr(uint32_t frames, uint32_t tokens_per_frame, uint32_t block_size,
+                                int kind, int sink, uint32_t grid_rows, const uint64_t* row_ptr,
+                                const uint32_t* col_idx, void* stream, radial_layout** out) {
+    if (!out || !row_ptr) return fail(RADIAL_ERR_INVALID, "null argument");
+    *out = nullptr;
+    int rc = check_shape(frames, tokens_per_frame, block_size);
+    if (rc) return rc;
+    if ((rc = check_pattern(kind, 0, 0, true, true))) return rc;
+    const uint64_t R = (static_cast<uint64_t>(frames) * tokens_per_frame + block_size - 1) / block_size;
+    if (grid_rows != R)
+        return fail(RADIAL_ERR_INVALID, "grid_rows: expected " + std::to_string(R) + " for this shape, got " +
+                                            std::to_string(grid_rows));
+    // validation as in deserialize (block.hpp:274-302)
+    if (row_ptr[0] != 0) return fail(RADIAL_ERR_INVALID, "row_ptr: must start at 0");
+    uint32_t mx = 0, mn = 0xffffffffu;
+    int64_t first_empty = -1;
+    for (uint64_t I = 0; I < R; ++I) {
+        if (row_ptr[I + 1] < row_ptr[I])
+            return fail(RADIAL_ERR_INVALID, "row_ptr: not nondecreasing at row " + std::to_string(I + 1));
+        const uint64_t len = row_ptr[I + 1] - row_ptr[I];
+        mx = std::max<uint32_t>(mx, static_cast<uint32_t>(std::min<uint64_t>(len, 0xffffffffu)));
+        mn = std::min<uint32_t>(mn, static_cast<uint32_t>(std::min<uint64_t>(len, 0xffffffffu)));
+        if (len == 0 && first_empty < 0) first_empty = static_cast<int64_t>(I);
+    }
+    const uint64_t nnz = row_ptr[R];
+    if (nnz > R * R) return fail(RADIAL_ERR_INVALID, "row_ptr: kept-block count exceeds grid capacity");
+    if (nnz && !col_idx) return fail(RADIAL_ERR_INVALID, "null col_idx");
+    for (uint64_t I = 0; I < R; ++I)
+        for (uint64_t e = row_ptr[I]; e < row_ptr[I + 1]; ++e) {
+            if (col_idx[e] >= R)
+                return fail(RADIAL_ERR_INVALID, "col_idx: column " + std::to_string(col_idx[e]) +
+                                                    " out of range at entry " + std::to_string(e));
+            if (e > row_ptr[I] && col_idx[e] <= col_idx[e - 1])
+                return fail(RADIAL_ERR_INVALID, "col_idx: not strictly increasing in row " + std::to_string(I));
+        }
+    auto* L = new radial_layout();
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    auto bail = [&](int code) {
+        free_layout(L);
+        return code;
+    };
+    if (cudaGetDevice(&L->device) != cudaSuccess) return bail(cuda_fail(cudaGetLastError(), "cudaGetDevice"));
+    L->f = frames;
+    L->s = tokens_per_frame;
+    L->B = block_size;
+    L->R = static_cast<uint32_t>(R);
+    L->kind = static_cast<uint8_t>(kind);
+    L->sink = sink ? 1 : 0;
+    L->nnz = nnz;
+    L->first_empty_row = first_empty;
+    L->max_row_len = R ? mx : 0;
+    L->min_row_len = R ? mn : 0;
+    cudaError_t e;
+    if ((e = cudaMalloc(&L->row_ptr, sizeof(uint64_t) * (R + 1))) != cudaSuccess) return bail(cuda_fail(e, "cudaMalloc"));
+    if ((e = cudaMalloc(&L->col_idx, sizeof(uint32_t) * std::max<uint64_t>(nnz, 1))) != cudaSuccess)
+        return bail(cuda_fail(e, "cudaMalloc"));
+    if ((e = cudaMemcpyAsync(L->row_ptr, row_ptr, sizeof(uint64_t) * (R + 1), cudaMemcpyHostToDevice, st)) != cudaSuccess)
+        return bail(cuda_fail(e, "cudaMemcpyAsync"));
+    if (nnz && (e = cudaMemcpyAsync(L->col_idx, col_idx, sizeof(uint32_t) * nnz, cudaMemcpyHostToDevice, st)) != cudaSuccess)
+        return bail(cuda_fail(e, "cudaMemcpyAsync"));
+    if ((rc = build_worklists(L, st))) return bail(rc);
+    *out = L;
+    return RADIAL_OK;
+}
+
+int radial_cuda_layout_info(const radial_layout* L, radial_layout_info* info) {
+    if (!L || !info) return fail(RADIAL_ERR_INVALID, "null argument");
+    info->frames = L->f;
+    info->tokens_per_frame = L->s;
+    info->block_size = L->B;
+    info->grid_rows = L->R;
+    info->kind = L->kind;
+    info->sink = L->sink;
+    info->kept_blocks = L->nnz;
+    info->first_empty_row = L->first_empty_row;
+    info->max_row_len = L->max_row_len;
+    info->min_row_len = L->min_row_len;
+    return RADIAL_OK;
+}
+
+int radial_cuda_layout_copy_csr(const radial_layout* L, uint64_t* row_ptr, uint32_t* col_idx) {
+    if (!L || !row_ptr) return fail(RADIAL_ERR_INVALID, "null argument");
+    RADIAL_CUDA_TRY(cudaMemcpy(row_ptr, L->row_ptr, sizeof(uint64_t) * (static_cast<size_t>(L->R) + 1),
+                               cudaMemcpyDeviceToHost));
+    if (L->nnz && col_idx)
+        RADIAL_CUDA_TRY(cudaMemcpy(col_idx, L->col_idx, sizeof(uint32_t) * L->nnz, cudaMemcpyDeviceToHost));
+    return RADIAL_OK;
+}
+
+int radial_cuda_layout_copy_csc(const radial_layout* L, uint64_t* col_ptr, uint32_t* row_idx) {
+    if (!L || !col_ptr) return fail(RADIAL_ERR_INVALID, "null argument");
+    RADIAL_CUDA_TRY(cudaMemcpy(col_ptr, L->col_ptr, sizeof(uint64_t) * (static_cast<size_t>(L->R) + 1),
+                               cudaMemcpyDeviceToHost));
+    if (L->nnz && row_idx)
+        RADIAL_CUDA_TRY(cudaMemcpy(row_idx, L->row_idx, sizeof(uint32_t) * L->nnz, cudaMemcpyDeviceToHost));
+    return RADIAL_OK;
+}
+
+int radial_cuda_layout_device_csr(const radial_layout* L, const uint64_t** row_ptr,
+                                  const uint32_t** col_idx) {
+    if (!L) return fail(RADIAL_ERR_INVALID, "null layout");
+    if (row_ptr) *row_ptr = L->row_ptr;
+    if (col_idx) *col_idx = L->col_idx;
+    return RADIAL_OK;
+}
+
+void radial_cuda_layout_free(radial_layout* L) { free_layout(L); }
+
+int radial_cuda_attn_fwd(const void* q, const void* k, const void* v, void* o, float* lse,
+                         uint32_t heads, uint64_t n, uint32_t head_dim, float scale,
+                         const radial_layout* layout, void* stream) {
+    int rc = check_attn(q, k, v, o, heads, n, head_dim);
+    if (rc) return rc;
+    if ((rc = check_layout_for_attn(layout, n))) return rc;
+    return launch_fwd(q, k, v, o, lse, heads, n, head_dim, layout->B, resolve_scale(scale, head_dim), layout,
+                      static_cast<cudaStream_t>(stream));
+}
+
+int radial_cuda_attn_fwd_dense(const void* q, const void* k, const void* v, void* o, float* lse,
+                               uint32_t heads, uint64_t n, uint32_t head_dim, uint32_t block_size,
+                               float scale, void* stream) {
+    int rc = check_attn(q, k, v, o, heads, n, head_dim);
+    if (rc) return rc;
+    if (block_size != 64 && block_size != 128)
+        return fail(RADIAL_ERR_INVALID, "dense_attention: block_size must be 64 or 128");
+    return launch_fwd(q, k, v, o, lse, heads, n, head_dim, block_size, resolve_scale(scale, head_dim),
+                      nullptr, static_cast<cudaStream_t>(stream));
+}
+
+int radial_cuda_attn_fwd_host(const void* q, const void* k, const void* v, void* o, float* lse,
+                              uint32_t heads, uint64_t n, uint32_t head_dim, float scale,
+                              const radial_layout* layout, void* stream) {
+    int rc = check_attn(q, k, v, o, heads, n, head_dim);
+    if (rc) return rc;
+    if ((rc = check_layout_for_attn(layout, n))) return rc;
+    // per-thread cached device workspace: q, k, v, o (bf16) + lse
+    thread_local void* ws = nullptr;
+    thread_local size_t ws_bytes = 0;
+    thread_local int ws_dev = -1;
+    int dev = 0;
+    RADIAL_CUDA_TRY(cudaGetDevice(&dev));
+    const size_t tbytes = static_cast<size_t>(heads) * n * head_dim * 2;
+    const size_t lbytes = static_cast<size_t>(heads) * n * 4;
+    const size_t need = 4 * tbytes + lbytes + 4096;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (ws_bytes < need || ws_dev != dev) {
+        if (ws) cudaFree(ws);
+        ws = nullptr;
+        ws_bytes = 0;
+        RADIAL_CUDA_TRY(cudaMalloc(&ws, need));
+        ws_bytes = need;
+        ws_dev = dev;
+    }
+    auto* base = static_cast<uint8_t*>(ws);
+    void* dq = base;
+    void* dk = base + tbytes;
+    void* dv = base + 2 * tbytes;
+    void* dO = base + 3 * tbytes;
+    float* dl = reinterpret_cast<float*>(base + 4 * tbytes);
+    RADIAL_CUDA_TRY(cudaMemcpyAsync(dq, q, tbytes, cudaMemcpyHostToDevice, st));
+    RADIAL_CUDA_TRY(cudaMemcpyAsync(dk, k, tbytes, cudaMemcpyHostToDevice, st));
+    RADIAL_CUDA_TRY(cudaMemcpyAsync(dv, v, tbytes, cudaMemcpyHostToDevice, st));
+    rc = launch_fwd(dq, dk, dv, dO, lse ? dl : nullptr, heads, n, head_dim, layout->B,
+                    resolve_scale(scale, head_dim), layout, st);
+    if (rc) return rc;
+    RADIAL_CUDA_TRY(cudaMemcpyAsync(o, dO, tbytes, cudaMemcpyDeviceToHost, st));
+    if (lse) RADIAL_CUDA_TRY(cudaMemcpyAsync(lse, dl, lbytes, cudaMemcpyDeviceToHost, st));
+    RADIAL_CUDA_TRY(cudaStreamSynchronize(st));
+    return RADIAL_OK;
+}
+
+size_t radial_cuda_attn_bwd_workspace_size(uint32_t heads, uint64_t n, uint32_t head_dim) {
+    return bwd_workspace_bytes(heads, n, head_dim);
+}
+
+int radial_cuda_attn_bwd(const void* q, const void* k, const void* v, const void* o, const float* lse,
+                         const void* dout, void* dq, void* dk, void* dv, uint32_t heads, uint64_t n,
+                         uint32_t head_dim, float scale, const radial_layout* layout, void* workspace,
+                         void* stream) {
+    int rc = check_attn(q, k, v, o, heads, n, head_dim);
+    if (rc) return rc;
+    if (!lse || !dout || !dq || !dk || !dv) return fail(RADIAL_ERR_INVALID, "attn_bwd: null tensor");
+    if ((rc = check_layout_for_attn(layout, n))) return rc;
+    return launch_bwd(q, k, v, o, lse, dout, dq, dk, dv, heads, n, head_dim, resolve_scale(scale, head_dim),
+                      layout, workspace, static_cast<cudaStream_t>(stream));
+}
+
+int radial_cuda_attention_flops(const radial_layout* L, uint32_t head_dim, uint32_t heads,
+                                double* dense_flops, double* sparse_flops, double* reduction) {
+    if (!L) return fail(RADIAL_ERR_INVALID, "null layout");
+    if (head_dim < 1) return fail(RADIAL_ERR_INVALID, "attention_flops: head_dim must be >= 1");
+    if (heads < 1) return fail(RADIAL_ERR_INVALID, "attention_flops: num_heads must be >= 1");
+    const double n = static_cast<double>(L->f) * L->s;
+    const double B = L->B;
+    const double dense = 4.0 * n * n * head_dim * heads;
+    const double sparse = 4.0 * static_cast<double>(L->nnz) * B * B * head_dim * heads;
+    if (dense_flops) *dense_flops = dense;
+    if (sparse_flops) *sparse_flops = sparse;
+    if (reduction) *reduction = dense / sparse;
+    return RADIAL_OK;
+}
+
+double radial_cuda_sparsity(const radial_layout* L) {
+    if (!L) return 0.0;
+    return 1.0 - static_cast<double>(L->nnz) / (static_cast<double>(L->R) * static_cast<double>(L->R));
+}
+
+}  // extern "C"

@@ -1,0 +1,57 @@
+// radial_internal.h -- host-side internals shared by the CUDA translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+
+#include "../../include/radial_cuda.h"
+
+// Device-resident block layout.  Everything the kernels need is built once
+// per (shape, pattern, block size) and is immutable afterwards.
+struct radial_layout {
+    int device = 0;
+    uint32_t f = 1, s = 1, B = 1, R = 0;
+    uint8_t kind = 0, sink = 1;
+    uint32_t tw = 0, sw = 0;
+    uint64_t nnz = 0;
+    int64_t first_empty_row = -1;
+    uint32_t max_row_len = 0, min_row_len = 0;
+
+    // CSR (BlockLayout::row_ptr / col_idx, bit-exact with the reference)
+    uint64_t* row_ptr = nullptr;  // [R+1]
+    uint32_t* col_idx = nullptr;  // [nnz]
+    // CSC: per-KV-block lists of query blocks (backward)
+    uint64_t* col_ptr = nullptr;  // [R+1]
+    uint32_t* row_idx = nullptr;  // [nnz]
+
+    // Forward work list: a chunk is 256 query rows = G = 256/B query blocks.
+    // uidx entries are J | (mask << 28), mask bit g set iff block chunk*G+g keeps J.
+    uint32_t G = 0, C = 0;        // blocks per chunk, number of chunks
+    uint64_t* uptr = nullptr;     // [C+1]
+    uint32_t* uidx = nullptr;
+    uint32_t* uorder = nullptr;   // chunks by descending list length (LPT)
+    // Backward dK/dV work list: same over KV chunks using the CSC.
+    uint64_t* tptr = nullptr;
+    uint32_t* tidx = nullptr;
+    uint32_t* torder = nullptr;
+};
+
+namespace radial_detail {
+
+void set_error(const std::string& msg);
+int fail(int code, const std::string& msg);
+int cuda_fail(cudaError_t e, const char* where);
+
+// mask_build.cu
+int build_layout_device(radial_layout* L, cudaStream_t st);
+int build_worklists(radial_layout* L, cudaStream_t st);
+
+}  // namespace radial_detail
+
+#define RADIAL_CUDA_TRY(expr)                                                   \
+    do {                                                                        \
+        cudaError_t e_ = (expr);                                                \
+        if (e_ != cudaSuccess) return radial_detail::cuda_fail(e_, #expr);      \
+    } while (0)

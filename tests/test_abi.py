@@ -1,0 +1,99 @@
+"""CPU tests: the C-ABI library loads and exports every symbol include/radial_cuda.h
+declares; host-side logic (serialization, accounting) matches the reference."""
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _declared_symbols():
+    with open(os.path.join(ROOT, "include", "radial_cuda.h")) as fh:
+        text = fh.read()
+    return sorted(set(re.findall(r"\b(radial_cuda_\w+)\s*\(", text)))
+
+
+def test_library_exports_every_declared_symbol():
+    import paper_2506_19852_b200 as P
+    lib = ctypes.CDLL(P.library_path())
+    syms = _declared_symbols()
+    assert len(syms) >= 15
+    missing = [s for s in syms if not hasattr(lib, s)]
+    assert not missing, missing
+    assert lib.radial_cuda_abi_version() == 1
+
+
+def test_library_is_sm100a():
+    import subprocess
+    import paper_2506_19852_b200 as P
+    out = subprocess.run(["cuobjdump", "--list-elf", P.library_path()], capture_output=True,
+                         text=True)
+    if out.returncode != 0:
+        pytest.skip("cuobjdump unavailable")
+    assert "sm_100a" in out.stdout
+
+
+def test_serialize_roundtrip_and_matches_oracle_bytes():
+    import oracle as O
+    import paper_2506_19852_b200 as P
+    rng = np.random.default_rng(23)
+    for _ in range(30):
+        f, s, B = (int(x) for x in (1 + rng.integers(12), 1 + rng.integers(12), 1 + rng.integers(9)))
+        sink = bool(rng.integers(2))
+        rp, ci = O.blockify(f, s, B, "radial", sink)
+        lay = P.BlockLayout(P.GridShape(f, s), B, len(rp) - 1, rp, ci, 0, sink)
+        data = P.serialize(lay)
+        assert data == O.serialize(f, s, B, "radial", sink, rp, ci)
+        assert P.deserialize(data) == lay
+
+
+def test_parse_errors_are_structured():
+    # test_blocksparse.cpp:172-217
+    import oracle as O
+    import paper_2506_19852_b200 as P
+    rp, ci = O.blockify(4, 4, 4)
+    good = P.serialize(P.BlockLayout(P.GridShape(4, 4), 4, 4, rp, ci))
+    cases = [(b"X" + good[1:], "magic"), (good[:4] + b"\x7f" + good[5:], "version"),
+             (good[:-1], "col_idx"), (good + b"\0", "trailer"),
+             (good[:18] + bytes([9]) + good[19:], "kind")]
+    for data, fieldname in cases:
+        with pytest.raises(P.ParseError, match=fieldname):
+            P.deserialize(data)
+    with pytest.raises(P.ParseError):
+        P.deserialize(good[:10])
+    with pytest.raises(P.ParseError) as ei:
+        P.deserialize(b"RAMK")
+    assert ei.value.field == "version"
+
+
+def test_attention_flops_and_sparsity_match_reference_convention():
+    import oracle as O
+    import paper_2506_19852_b200 as P
+    rp, ci = O.blockify(33, 3600, 128)
+    lay = P.BlockLayout(P.GridShape(33, 3600), 128, len(rp) - 1, rp, ci)
+    rep = P.attention_flops(lay, 128, 24)
+    assert rep.sparse_flops == pytest.approx(7.8399e13, rel=1e-4)
+    assert rep.dense_flops == pytest.approx(1.73426e14, rel=1e-4)
+    assert P.sparsity(lay) == pytest.approx(0.5488, abs=1e-4)
+    if O.ref_available():
+        d, sp, red, spars = (ctypes.c_double() for _ in range(4))
+        assert O.ref().ref_attention_flops(33, 3600, 128, 1, 128, 24, ctypes.byref(d),
+                                           ctypes.byref(sp), ctypes.byref(red),
+                                           ctypes.byref(spars)) == 0
+        assert rep.sparse_flops == sp.value and rep.dense_flops == d.value
+        assert P.sparsity(lay) == spars.value
+    with pytest.raises(ValueError):
+        P.attention_flops(lay, 0, 1)
+
+
+def test_grid_shape_and_pattern_validation():
+    import paper_2506_19852_b200 as P
+    with pytest.raises(ValueError):
+        P.GridShape(0, 4)
+    with pytest.raises(ValueError):
+        P.GridShape(1 << 20, 1 << 13)
+    with pytest.raises(ValueError, match="temporal_window"):
+        P.PatternSpec(P.PatternKind.sta, False, None, 2).validate()

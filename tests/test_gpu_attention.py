@@ -1,0 +1,183 @@
+"""GPU parity: K2 sparse forward and K4 dense forward against the fp64 oracle (and the
+reference itself where it is cheap), per (head, query block)."""
+import numpy as np
+import pytest
+
+import oracle as O
+from tests._util import (assert_within, bf16_bits, bits_to_f32, block_errors, instance_bf16,
+                         to_torch_bf16)
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def P():
+    import torch
+    assert torch.cuda.is_available(), "GPU test on a box without CUDA"
+    import paper_2506_19852_b200 as P
+    return P
+
+
+def _run_sparse(P, f, s, B, d, H, sink=True, q_scale=1.0, seed0=42):
+    import torch
+    q, k, v = instance_bf16(f, s, d, H, seed0, q_scale)
+    lay = P.device_layout(P.GridShape(f, s), P.PatternSpec.radial(sink), B)
+    o, lse = P.masked_attention(to_torch_bf16(q), to_torch_bf16(k), to_torch_bf16(v), lay,
+                                return_lse=True)
+    torch.cuda.synchronize()
+    return q, k, v, lay.host(), o.float().cpu().numpy(), lse.cpu().numpy()
+
+
+def test_debug_tile_mma_building_blocks(P):
+    """S = Q K^T (SS, K-major) and O = P V (TS, MN-major V) on one 128x128x128 tile."""
+    import ctypes
+    import torch
+    lib = ctypes.CDLL(P.library_path())
+    g = torch.Generator(device="cuda").manual_seed(0)
+    q, k, v, p = (torch.randn(128, 128, device="cuda", generator=g).to(torch.bfloat16) for _ in range(4))
+    s_out = torch.empty(128, 128, device="cuda")
+    o_out = torch.empty(128, 128, device="cuda")
+    rc = lib.radial_cuda_debug_tile(ctypes.c_void_p(q.data_ptr()), ctypes.c_void_p(k.data_ptr()),
+                                    ctypes.c_void_p(v.data_ptr()), ctypes.c_void_p(p.data_ptr()),
+                                    ctypes.c_void_p(s_out.data_ptr()), ctypes.c_void_p(o_out.data_ptr()),
+                                    ctypes.c_void_p(0))
+    assert rc == 0
+    torch.cuda.synchronize()
+    s_ref = q.float() @ k.float().T
+    o_ref = p.float() @ v.float()
+    es = (s_out - s_ref).abs().max().item()
+    eo = (o_out - o_ref).abs().max().item()
+    assert es < 1e-2 * s_ref.abs().max().item(), f"S mismatch {es}"
+    assert eo < 1e-2 * o_ref.abs().max().item(), f"O mismatch {eo}"
+
+
+def test_tiny_config_vs_oracle_all_rows(P):
+    # BASELINE configs[0]: 8 frames x 256 tokens, 2 heads, head_dim 64, block 64
+    f, s, B, d, H = 8, 256, 64, 64, 2
+    q, k, v, host, o, lse = _run_sparse(P, f, s, B, d, H)
+    n = f * s
+    rows = np.arange(n)
+    for h in range(H):
+        want, wl = O.attention_rows(q[h], k[h], v[h], B, host.row_ptr, host.col_idx, rows,
+                                    want_lse=True)
+        assert_within(block_errors(o[h], want, rows, B), f"tiny head {h}")
+        assert np.abs(lse[h] - wl).max() < 2e-2
+
+
+@pytest.mark.skipif(not O.ref_available(), reason="oracle/_ref not built")
+def test_tiny_config_vs_reference_library(P):
+    """The reference's own masked_attention on the same bf16-rounded inputs."""
+    f, s, B, d = 8, 256, 64, 64
+    q, k, v, host, o, _ = _run_sparse(P, f, s, B, d, 1)
+    ref = O.ref_masked_attention(f, s, q[0].astype(np.float64), k[0].astype(np.float64),
+                                 v[0].astype(np.float64), B, host.row_ptr, host.col_idx)
+    assert_within(block_errors(o[0], ref, np.arange(f * s), B), "tiny vs reference")
+
+
+@pytest.mark.parametrize("f,s,B,d", [(5, 300, 128, 128), (3, 1000, 128, 128), (7, 200, 64, 128),
+                                     (4, 333, 128, 64), (2, 64, 64, 64), (1, 100, 128, 128),
+                                     (9, 130, 64, 64), (12, 257, 128, 128)])
+@pytest.mark.parametrize("sink", [True, False])
+def test_ragged_shapes_vs_oracle(P, f, s, B, d, sink):
+    H = 2
+    q, k, v, host, o, lse = _run_sparse(P, f, s, B, d, H, sink=sink, seed0=7)
+    rows = np.arange(f * s)
+    for h in range(H):
+        want, wl = O.attention_rows(q[h], k[h], v[h], B, host.row_ptr, host.col_idx, rows,
+                                    want_lse=True)
+        assert_within(block_errors(o[h], want, rows, B), f"f{f}s{s}B{B}d{d} head {h}")
+        assert np.abs(lse[h] - wl).max() < 2e-2
+
+
+@pytest.mark.parametrize("B,d", [(128, 128), (64, 64)])
+def test_peaked_logits_q_times_8(P, B, d):
+    f, s, H = 6, 400, 2
+    q, k, v, host, o, _ = _run_sparse(P, f, s, B, d, H, q_scale=8.0, seed0=3)
+    rows = np.arange(f * s)
+    for h in range(H):
+        want = O.attention_rows(q[h], k[h], v[h], B, host.row_ptr, host.col_idx, rows)
+        assert_within(block_errors(o[h], want, rows, B), f"peaked head {h}")
+
+
+@pytest.mark.parametrize("n,d,B", [(1500, 128, 128), (2048, 64, 64), (700, 128, 64)])
+def test_dense_kernel_vs_oracle(P, n, d, B):
+    import torch
+    H = 2
+    q, k, v = instance_bf16(1, n, d, H, 11)
+    o = P.dense_attention(to_torch_bf16(q), to_torch_bf16(k), to_torch_bf16(v), block_size=B)
+    torch.cuda.synchronize()
+    o = o.float().cpu().numpy()
+    rows = np.arange(n)
+    for h in range(H):
+        want = O.attention_rows(q[h], k[h], v[h], B, None, None, rows)
+        assert_within(block_errors(o[h], want, rows, B), f"dense n{n} head {h}")
+
+
+def test_dense_pattern_layout_equals_dense_kernel(P):
+    """masked_attention over the dense PatternSpec == the dense comparator (acceptance crit. 5)."""
+    import torch
+    f, s, d, H = 4, 300, 128, 2
+    q, k, v = (to_torch_bf16(x) for x in instance_bf16(f, s, d, H, 5))
+    lay = P.device_layout(P.GridShape(f, s), P.PatternSpec.dense(), 128)
+    a = P.masked_attention(q, k, v, lay)
+    b = P.dense_attention(q, k, v, block_size=128)
+    torch.cuda.synchronize()
+    assert torch.equal(a, b)
+
+
+def test_host_buffer_api_matches_device_path(P):
+    import torch
+    f, s, B, d, H = 8, 256, 64, 64, 2
+    q, k, v = instance_bf16(f, s, d, H, 42)
+    lay = P.device_layout(P.GridShape(f, s), P.PatternSpec.radial(), B)
+    dev = P.masked_attention(to_torch_bf16(q), to_torch_bf16(k), to_torch_bf16(v), lay)
+    torch.cuda.synchronize()
+    host = P.masked_attention_host(bf16_bits(q), bf16_bits(k), bf16_bits(v), lay)
+    assert np.array_equal(host, dev.view(torch.int16).cpu().numpy().view(np.uint16))
+
+
+def test_errors_follow_reference_semantics(P):
+    import torch
+    q = torch.zeros(1, 16, 64, device="cuda", dtype=torch.bfloat16)
+    # fully masked rows: attention.hpp:255-258 ("row 0"), test_attention.cpp:143-154
+    empty = P.BlockLayout(P.GridShape(1, 16), 64, 1, np.zeros(2, np.uint64), np.zeros(0, np.uint32))
+    with pytest.raises(RuntimeError, match="row 0"):
+        P.masked_attention(q, q, q, empty)
+    lay = P.device_layout(P.GridShape(2, 8), P.PatternSpec.radial(), 64)
+    with pytest.raises(ValueError, match="shape mismatch"):
+        P.masked_attention(torch.zeros(1, 32, 64, device="cuda", dtype=torch.bfloat16),
+                           torch.zeros(1, 32, 64, device="cuda", dtype=torch.bfloat16),
+                           torch.zeros(1, 32, 64, device="cuda", dtype=torch.bfloat16), lay)
+    q32 = torch.zeros(1, 16, 32, device="cuda", dtype=torch.bfloat16)
+    lay16 = P.device_layout(P.GridShape(1, 16), P.PatternSpec.radial(), 64)
+    with pytest.raises(ValueError, match="head_dim"):
+        P.masked_attention(q32, q32, q32, lay16)
+    lay_b4 = P.device_layout(P.GridShape(1, 16), P.PatternSpec.radial(), 4)
+    with pytest.raises(ValueError, match="block_size"):
+        P.masked_attention(q, q, q, lay_b4)
+
+
+def test_paper_scale_hunyuan33_sampled_blocks(P):
+    """BASELINE configs[1] at full size: every head computed on the GPU; a sample of
+    (head, query block) pairs -- first, tail, sink-adjacent and random -- checked
+    against the fp64 oracle on the same bf16 inputs (rows are independent)."""
+    import torch
+    f, s, B, d, H = 33, 3600, 128, 128, 24
+    n = f * s
+    g = torch.Generator(device="cuda").manual_seed(1234)
+    q = torch.randn(H, n, d, device="cuda", generator=g).to(torch.bfloat16)
+    k = torch.randn(H, n, d, device="cuda", generator=g).to(torch.bfloat16)
+    v = torch.randn(H, n, d, device="cuda", generator=g).to(torch.bfloat16)
+    lay = P.device_layout(P.GridShape(f, s), P.PatternSpec.radial(), B)
+    o = P.masked_attention(q, k, v, lay)
+    torch.cuda.synchronize()
+    host = lay.host()
+    R = host.grid_rows
+    rng = np.random.default_rng(0)
+    for h in (0, 23):
+        blocks = sorted({0, 1, 28, R // 2, R - 2, R - 1} | set(rng.integers(0, R, 4).tolist()))
+        rows = np.concatenate([np.arange(I * B, min(n, (I + 1) * B)) for I in blocks])
+        qh, kh, vh = (x[h].float().cpu().numpy() for x in (q, k, v))
+        want = O.attention_rows(qh, kh, vh, B, host.row_ptr, host.col_idx, rows)
+        got = o[h].float().cpu().numpy()[rows]
+        assert_within(block_errors(got, want, rows, B), f"H33 head {h}")
