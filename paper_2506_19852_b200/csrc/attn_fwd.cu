@@ -35,6 +35,7 @@ constexpr int kBQ = 128;        // query rows per tile
 constexpr int kStagesK = 2;
 constexpr int kStagesV = 2;
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
+constexpr int kPolyOf8 = 3;                // columns per 8 using the polynomial exp2
 
 struct FwdParams {
     __nv_bfloat16* o;
@@ -94,10 +95,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
 
-    // work item: all heads of the longest chunks first (LPT)
+    // work item: head-major so the CTAs resident at any time share one head's K/V in L2
+    // (K+V of a head = 2 n d bytes = 61 MB at n = 118,800); longest chunks first within a
+    // head (LPT) so the tail of the grid is short.
     const uint32_t item = blockIdx.x;
-    const uint32_t head = item % p.heads;
-    const uint32_t chunk = p.order ? p.order[item / p.heads] : item / p.heads;
+    const uint32_t head = item / p.C;
+    const uint32_t chunk = p.order ? p.order[item % p.C] : item % p.C;
     const uint64_t row0 = static_cast<uint64_t>(chunk) * 256;
     uint64_t ebase = 0;
     uint32_t L;
@@ -139,11 +142,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
-
+    // producer / MMA / allocator warpgroup needs few registers; the two softmax
+    // warpgroups hold a 128-column S row each (384 x 168 = 128 x 56 + 256 x 224)
+    if (warp < 4) {
+        regs_dec<56>();
     if (warp == 0) {
         // ------------------------------------------------------------ producer
         if (lane == 0) {
-            const uint64_t pol_kv = l2_policy_evict_last();
             mbar_arrive_expect_tx(bar_q, 2 * Cfg::kQBytes);
             for (int t = 0; t < 2; ++t)
                 for (int a = 0; a < Cfg::kAtoms; ++a)
@@ -156,14 +161,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                 mbar_arrive_expect_tx(&bar_kfull[ks], Cfg::kKVBytes);
                 uint8_t* kd = smem + Cfg::kSmemK + ks * Cfg::kKVBytes;
                 for (int a = 0; a < Cfg::kAtoms; ++a)
-                    tma_load_3d_hint(kd + a * Cfg::kKVAtomBytes, &tm_k, &bar_kfull[ks], a * 64, J * BK,
-                                     head, pol_kv);
+                    tma_load_3d(kd + a * Cfg::kKVAtomBytes, &tm_k, &bar_kfull[ks], a * 64, J * BK, head);
                 mbar_wait(&bar_vempty[vs], ((j / kStagesV) & 1) ^ 1);
                 mbar_arrive_expect_tx(&bar_vfull[vs], Cfg::kKVBytes);
                 uint8_t* vd = smem + Cfg::kSmemV + vs * Cfg::kKVBytes;
                 for (int a = 0; a < Cfg::kAtoms; ++a)
-                    tma_load_3d_hint(vd + a * Cfg::kKVAtomBytes, &tm_v, &bar_vfull[vs], a * 64, J * BK,
-                                     head, pol_kv);
+                    tma_load_3d(vd + a * Cfg::kKVAtomBytes, &tm_v, &bar_vfull[vs], a * 64, J * BK, head);
             }
         }
     } else if (warp == 1) {
@@ -229,7 +232,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             mma_commit(&bar_ofull[0]);
             mma_commit(&bar_ofull[1]);
         }
-    } else if (warp >= 4) {
+    }
+    } else {
+        regs_inc<224>();
         // ------------------------------------------------------------ softmax
         const int t = (warp - 4) >> 2;                 // Q tile
         const int r = ((warp & 3) << 5) + lane;        // row in tile = TMEM lane
@@ -261,9 +266,15 @@ __global__ void __launch_bounds__(kThreads, 1)
             const bool active = (mask >> my_bit) & 1;
             const uint64_t kv0 = static_cast<uint64_t>(J) * BK;
             const int valid = (kv0 + BK <= p.n) ? BK : static_cast<int>(p.n - kv0);
+            const bool full = active && valid == BK;  // common case: no per-column masking
             float mx = -INFINITY;
+            if (full) {
 #pragma unroll
-            for (int c = 0; c < BK; ++c) mx = fmaxf(mx, c < valid ? s[c] : -INFINITY);
+                for (int c = 0; c < BK; ++c) mx = fmaxf(mx, s[c]);
+            } else if (active) {
+#pragma unroll
+                for (int c = 0; c < BK; ++c) mx = fmaxf(mx, c < valid ? s[c] : -INFINITY);
+            }
             const float m_cand = mx * sl2;
             const bool need = active && (m == -INFINITY || m_cand > m + kRescaleThreshold);
             const bool rescale = need && m != -INFINITY;
@@ -283,13 +294,32 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (need) m = m_cand;
             uint32_t pk[BK / 2];
             float rs = 0.f;
-            const float mb = active ? m : 0.f;
+            if (full) {
+                // FA4-style split: kPolyOf8 of every 8 columns use a cubic exp2 on the FMA
+                // pipe, the rest MUFU.EX2, so the two pipes share the 16K exps per tile.
+                float r0 = 0.f, r1 = 0.f;
+                const float nm = -m;
 #pragma unroll
-            for (int c = 0; c < BK; c += 2) {
-                float p0 = (active && c < valid) ? ex2(fmaf(s[c], sl2, -mb)) : 0.f;
-                float p1 = (active && c + 1 < valid) ? ex2(fmaf(s[c + 1], sl2, -mb)) : 0.f;
-                rs += p0 + p1;
-                pk[c / 2] = pack_bf16(p0, p1);
+                for (int c = 0; c < BK; c += 2) {
+                    const float x0 = fmaf(s[c], sl2, nm), x1 = fmaf(s[c + 1], sl2, nm);
+                    const float p0 = ((c & 7) < kPolyOf8) ? ex2_poly(x0) : ex2(x0);
+                    const float p1 = (((c + 1) & 7) < kPolyOf8) ? ex2_poly(x1) : ex2(x1);
+                    r0 += p0;
+                    r1 += p1;
+                    pk[c / 2] = pack_bf16(p0, p1);
+                }
+                rs = r0 + r1;
+            } else if (active) {
+#pragma unroll
+                for (int c = 0; c < BK; c += 2) {
+                    const float p0 = c < valid ? ex2(fmaf(s[c], sl2, -m)) : 0.f;
+                    const float p1 = c + 1 < valid ? ex2(fmaf(s[c + 1], sl2, -m)) : 0.f;
+                    rs += p0 + p1;
+                    pk[c / 2] = pack_bf16(p0, p1);
+                }
+            } else {
+#pragma unroll
+                for (int c = 0; c < BK / 2; ++c) pk[c] = 0u;
             }
             l += rs;
 #pragma unroll

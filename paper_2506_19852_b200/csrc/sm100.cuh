@@ -194,11 +194,32 @@ __host__ __device__ constexpr uint32_t idesc_bf16(int M, int N, int a_mn_major, 
            | (static_cast<uint32_t>(M >> 4) << 24);     // M / 16
 }
 
+// Per-warpgroup register re-allocation (all 4 warps of the warpgroup execute it).
+template <uint32_t N>
+__device__ __forceinline__ void regs_dec() {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(N));
+}
+template <uint32_t N>
+__device__ __forceinline__ void regs_inc() {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(N));
+}
+
 // ---------------------------------------------------------------- math
 __device__ __forceinline__ float ex2(float x) {
     float y;
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
     return y;
+}
+// 2^x on the FMA pipe (Cody-Waite split + cubic on [-1/2, 1/2], max rel err 1.0e-4,
+// well under bf16's 3.9e-3): for x in [-125, 126].  Used for a share of the softmax
+// exponentials so MUFU.EX2 is not the only exp2 pipe.
+__device__ __forceinline__ float ex2_poly(float x) {
+    x = fmaxf(x, -125.0f);
+    const float magic = 12582912.0f;  // 1.5 * 2^23: x + magic rounds x to an integer
+    const float t = x + magic;
+    const float f = x - (t - magic);
+    const float q = fmaf(fmaf(fmaf(0.05500859f, f, 0.24221037f), f, 0.6932829f), f, 1.0f);
+    return __int_as_float(__float_as_int(q) + (__float_as_int(t) << 23));
 }
 __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
     __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
