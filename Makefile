@@ -31,3 +31,8 @@ clean:
 	$(MAKE) -C oracle clean
 
 .PHONY: all lib oracle clean
+
+# kernel-variant libraries for tuning sweeps: make variant V=poly2 DEFS="-DRADIAL_POLY_PAIRS=2"
+variant:
+	@mkdir -p variants/$(V)
+	$(NVCC) $(NVFLAGS) $(DEFS) -shared -o variants/$(V)/libradial_cuda.so $(SRCS) 2> variants/$(V)/ptxas.log || (cat variants/$(V)/ptxas.log; exit 1)

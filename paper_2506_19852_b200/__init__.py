@@ -45,7 +45,8 @@ __all__ = [
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-_LIB_PATH = os.path.join(_HERE, "lib", "libradial_cuda.so")
+# RADIAL_CUDA_LIB overrides the in-tree library (used for kernel-variant sweeps)
+_LIB_PATH = os.environ.get("RADIAL_CUDA_LIB") or os.path.join(_HERE, "lib", "libradial_cuda.so")
 
 
 def library_path() -> str:

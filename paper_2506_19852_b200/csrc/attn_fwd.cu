@@ -35,7 +35,10 @@ constexpr int kBQ = 128;        // query rows per tile
 constexpr int kStagesK = 2;
 constexpr int kStagesV = 2;
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
-constexpr int kPolyOf8 = 3;                // columns per 8 using the polynomial exp2
+#ifndef RADIAL_POLY_PAIRS
+#define RADIAL_POLY_PAIRS 1
+#endif
+constexpr int kPolyPairs = RADIAL_POLY_PAIRS;  // column pairs per 4 using the polynomial exp2
 
 struct FwdParams {
     __nv_bfloat16* o;
@@ -129,7 +132,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         for (int t = 0; t < 2; ++t) {
             mbar_init(&bar_sfull[t], 1);
-            mbar_init(&bar_pready[t], 128);
+            mbar_init(&bar_pready[t], 4);  // one elected arrive per softmax warp
             mbar_init(&bar_ofull[t], 1);
         }
         fence_barrier_init();
@@ -295,20 +298,25 @@ __global__ void __launch_bounds__(kThreads, 1)
             uint32_t pk[BK / 2];
             float rs = 0.f;
             if (full) {
-                // FA4-style split: kPolyOf8 of every 8 columns use a cubic exp2 on the FMA
-                // pipe, the rest MUFU.EX2, so the two pipes share the 16K exps per tile.
-                float r0 = 0.f, r1 = 0.f;
-                const float nm = -m;
+                // FA4-style split: kPolyPairs of every 4 column pairs use a cubic exp2 on
+                // the FMA pipe, the rest MUFU.EX2, so both pipes share the 16K exps per
+                // tile; scale, polynomial and row sums run as packed f32x2 ops.
+                float2 r2 = make_float2(0.f, 0.f);
+                const float2 sl = make_float2(sl2, sl2), nm = make_float2(-m, -m);
 #pragma unroll
                 for (int c = 0; c < BK; c += 2) {
-                    const float x0 = fmaf(s[c], sl2, nm), x1 = fmaf(s[c + 1], sl2, nm);
-                    const float p0 = ((c & 7) < kPolyOf8) ? ex2_poly(x0) : ex2(x0);
-                    const float p1 = (((c + 1) & 7) < kPolyOf8) ? ex2_poly(x1) : ex2(x1);
-                    r0 += p0;
-                    r1 += p1;
-                    pk[c / 2] = pack_bf16(p0, p1);
+                    const float2 x = __ffma2_rn(make_float2(s[c], s[c + 1]), sl, nm);
+                    float2 pr;
+                    if (((c >> 1) & 3) < kPolyPairs) {
+                        pr = ex2_poly2(x);
+                    } else {
+                        pr.x = ex2(x.x);
+                        pr.y = ex2(x.y);
+                    }
+                    r2 = __fadd2_rn(r2, pr);
+                    pk[c / 2] = pack_bf16(pr.x, pr.y);
                 }
-                rs = r0 + r1;
+                rs = r2.x + r2.y;
             } else if (active) {
 #pragma unroll
                 for (int c = 0; c < BK; c += 2) {
@@ -326,7 +334,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int c = 0; c < BK / 2; c += 16) tmem_st16(s_addr + c, pk + c);
             tmem_wait_st();
             tc_fence_before();
-            mbar_arrive(&bar_pready[t]);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&bar_pready[t]);
         }
         // ------------------------------------------------------------ epilogue
         mbar_wait(&bar_ofull[t], 0);

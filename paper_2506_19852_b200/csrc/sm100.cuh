@@ -221,6 +221,19 @@ __device__ __forceinline__ float ex2_poly(float x) {
     const float q = fmaf(fmaf(fmaf(0.05500859f, f, 0.24221037f), f, 0.6932829f), f, 1.0f);
     return __int_as_float(__float_as_int(q) + (__float_as_int(t) << 23));
 }
+// Packed-pair variant on the sm_100 f32x2 FMA path (FFMA2/FADD2: two lanes per issue).
+__device__ __forceinline__ float2 ex2_poly2(float2 x) {
+    const float2 magic = make_float2(12582912.0f, 12582912.0f);
+    x.x = fmaxf(x.x, -125.0f);
+    x.y = fmaxf(x.y, -125.0f);
+    const float2 t = __fadd2_rn(x, magic);
+    const float2 f = __fadd2_rn(x, __fadd2_rn(magic, make_float2(-t.x, -t.y)));
+    float2 q = __ffma2_rn(make_float2(0.05500859f, 0.05500859f), f, make_float2(0.24221037f, 0.24221037f));
+    q = __ffma2_rn(q, f, make_float2(0.6932829f, 0.6932829f));
+    q = __ffma2_rn(q, f, make_float2(1.0f, 1.0f));
+    return make_float2(__int_as_float(__float_as_int(q.x) + (__float_as_int(t.x) << 23)),
+                       __int_as_float(__float_as_int(q.y) + (__float_as_int(t.y) << 23)));
+}
 __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
     __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
     return *reinterpret_cast<uint32_t*>(&v);
