@@ -32,7 +32,10 @@ namespace {
 
 constexpr int kThreads = 384;
 constexpr int kBQ = 128;        // query rows per tile
-constexpr int kStagesK = 2;
+#ifndef RADIAL_STAGES_K
+#define RADIAL_STAGES_K 2
+#endif
+constexpr int kStagesK = RADIAL_STAGES_K;
 constexpr int kStagesV = 2;
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
 #ifndef RADIAL_POLY_PAIRS
@@ -65,7 +68,7 @@ struct FwdCfg {
     static constexpr int kSmemK = kSmemQ + 2 * kQBytes;
     static constexpr int kSmemV = kSmemK + kStagesK * kKVBytes;
     static constexpr int kSmemBar = kSmemV + kStagesV * kKVBytes;
-    static constexpr int kNumBars = 1 + 2 * kStagesK + 2 * kStagesV + 2 + 2 + 2;
+    static constexpr int kNumBars = 1 + 2 * kStagesK + 2 * kStagesV + 2 + 4 + 2;
     static constexpr int kSmemBytes = kSmemBar + kNumBars * 8 + 16;
     static constexpr int kSmemAlloc = kSmemBytes + 1024;  // slack for 1024 B alignment
     // TMEM columns
@@ -91,8 +94,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint64_t* bar_vfull = bar_kempty + kStagesK;
     uint64_t* bar_vempty = bar_vfull + kStagesV;
     uint64_t* bar_sfull = bar_vempty + kStagesV;  // [2]
-    uint64_t* bar_pready = bar_sfull + 2;          // [2]
-    uint64_t* bar_ofull = bar_pready + 2;          // [2]
+    uint64_t* bar_pready = bar_sfull + 2;          // [2 tiles][2 key halves]
+    uint64_t* bar_ofull = bar_pready + 4;          // [2]
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar_ofull + 2);
 
     const int warp = threadIdx.x >> 5;
@@ -132,7 +135,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         for (int t = 0; t < 2; ++t) {
             mbar_init(&bar_sfull[t], 1);
-            mbar_init(&bar_pready[t], 4);  // one elected arrive per softmax warp
+            mbar_init(&bar_pready[2 * t], 4);  // one elected arrive per softmax warp
+            mbar_init(&bar_pready[2 * t + 1], 4);
             mbar_init(&bar_ofull[t], 1);
         }
         fence_barrier_init();
@@ -198,19 +202,22 @@ __global__ void __launch_bounds__(kThreads, 1)
                 tc_fence_after();
                 for (int t = 0; t < 2; ++t) {
                     if (pend[t]) {
-                        mbar_wait(&bar_pready[t], pphase[t]);
-                        pphase[t] ^= 1;
-                        tc_fence_after();
                         const uint32_t vb = v_base + ((j - 1) % kStagesV) * Cfg::kKVBytes;
                         const uint32_t p_col = t ? Cfg::kColS1 : Cfg::kColS0;
                         const uint32_t o_col = t ? Cfg::kColO1 : Cfg::kColO0;
 #pragma unroll
-                        for (int kk = 0; kk < BK / 16; ++kk) {
-                            const uint64_t bdesc =
-                                sdesc_sw128(vb + kk * 16 * 128, Cfg::kKVAtomBytes, 1024);
-                            mma_ts(tmem + o_col, tmem + p_col + kk * 8, bdesc, Cfg::kIdescO,
-                                   (acc[t] | kk) ? 1u : 0u);
+                        for (int h = 0; h < 2; ++h) {
+                            mbar_wait(&bar_pready[2 * t + h], pphase[t]);
+                            tc_fence_after();
+#pragma unroll
+                            for (int kk = h * (BK / 32); kk < (h + 1) * (BK / 32); ++kk) {
+                                const uint64_t bdesc =
+                                    sdesc_sw128(vb + kk * 16 * 128, Cfg::kKVAtomBytes, 1024);
+                                mma_ts(tmem + o_col, tmem + p_col + kk * 8, bdesc, Cfg::kIdescO,
+                                       (acc[t] | kk) ? 1u : 0u);
+                            }
                         }
+                        pphase[t] ^= 1;
                         acc[t] = 1;
                         pend[t] = false;
                     }
@@ -272,8 +279,16 @@ __global__ void __launch_bounds__(kThreads, 1)
             const bool full = active && valid == BK;  // common case: no per-column masking
             float mx = -INFINITY;
             if (full) {
+                // tree reduction: 8 independent chains instead of one 128-long chain
+                float mm[8];
 #pragma unroll
-                for (int c = 0; c < BK; ++c) mx = fmaxf(mx, s[c]);
+                for (int x = 0; x < 8; ++x) mm[x] = s[x];
+#pragma unroll
+                for (int c = 8; c < BK; c += 8)
+#pragma unroll
+                    for (int x = 0; x < 8; ++x) mm[x] = fmaxf(mm[x], s[c + x]);
+                mx = fmaxf(fmaxf(fmaxf(mm[0], mm[1]), fmaxf(mm[2], mm[3])),
+                           fmaxf(fmaxf(mm[4], mm[5]), fmaxf(mm[6], mm[7])));
             } else if (active) {
 #pragma unroll
                 for (int c = 0; c < BK; ++c) mx = fmaxf(mx, c < valid ? s[c] : -INFINITY);
@@ -295,47 +310,55 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (rescale) l *= alpha;
             }
             if (need) m = m_cand;
-            uint32_t pk[BK / 2];
-            float rs = 0.f;
-            if (full) {
-                // FA4-style split: kPolyPairs of every 4 column pairs use a cubic exp2 on
-                // the FMA pipe, the rest MUFU.EX2, so both pipes share the 16K exps per
-                // tile; scale, polynomial and row sums run as packed f32x2 ops.
-                float2 r2 = make_float2(0.f, 0.f);
-                const float2 sl = make_float2(sl2, sl2), nm = make_float2(-m, -m);
+            // P is produced in two key halves, each published on its own barrier, so
+            // the MMA warp starts the first half of PV while the second half's
+            // exponentials are still being computed.
+            float2 r2a = make_float2(0.f, 0.f), r2b = make_float2(0.f, 0.f);
+            const float2 sl = make_float2(sl2, sl2), nm = make_float2(-m, -m);
 #pragma unroll
-                for (int c = 0; c < BK; c += 2) {
-                    const float2 x = __ffma2_rn(make_float2(s[c], s[c + 1]), sl, nm);
-                    float2 pr;
-                    if (((c >> 1) & 3) < kPolyPairs) {
-                        pr = ex2_poly2(x);
-                    } else {
-                        pr.x = ex2(x.x);
-                        pr.y = ex2(x.y);
+            for (int h = 0; h < 2; ++h) {
+                uint32_t pk[BK / 4];
+                if (full) {
+                    // FA4-style split: kPolyPairs of every 4 column pairs use a cubic exp2
+                    // on the FMA pipe, the rest MUFU.EX2; scale, polynomial and row sums
+                    // run as packed f32x2 ops.
+#pragma unroll
+                    for (int c = h * (BK / 2); c < (h + 1) * (BK / 2); c += 2) {
+                        const float2 x = __ffma2_rn(make_float2(s[c], s[c + 1]), sl, nm);
+                        float2 pr;
+                        if (((c >> 1) & 3) < kPolyPairs) {
+                            pr = ex2_poly2(x);
+                        } else {
+                            pr.x = ex2(x.x);
+                            pr.y = ex2(x.y);
+                        }
+                        if ((c >> 1) & 1)
+                            r2b = __fadd2_rn(r2b, pr);
+                        else
+                            r2a = __fadd2_rn(r2a, pr);
+                        pk[(c - h * (BK / 2)) / 2] = pack_bf16(pr.x, pr.y);
                     }
-                    r2 = __fadd2_rn(r2, pr);
-                    pk[c / 2] = pack_bf16(pr.x, pr.y);
-                }
-                rs = r2.x + r2.y;
-            } else if (active) {
+                } else if (active) {
 #pragma unroll
-                for (int c = 0; c < BK; c += 2) {
-                    const float p0 = c < valid ? ex2(fmaf(s[c], sl2, -m)) : 0.f;
-                    const float p1 = c + 1 < valid ? ex2(fmaf(s[c + 1], sl2, -m)) : 0.f;
-                    rs += p0 + p1;
-                    pk[c / 2] = pack_bf16(p0, p1);
-                }
-            } else {
+                    for (int c = h * (BK / 2); c < (h + 1) * (BK / 2); c += 2) {
+                        const float p0 = c < valid ? ex2(fmaf(s[c], sl2, -m)) : 0.f;
+                        const float p1 = c + 1 < valid ? ex2(fmaf(s[c + 1], sl2, -m)) : 0.f;
+                        r2a.x += p0;
+                        r2a.y += p1;
+                        pk[(c - h * (BK / 2)) / 2] = pack_bf16(p0, p1);
+                    }
+                } else {
 #pragma unroll
-                for (int c = 0; c < BK / 2; ++c) pk[c] = 0u;
+                    for (int c = 0; c < BK / 4; ++c) pk[c] = 0u;
+                }
+#pragma unroll
+                for (int c = 0; c < BK / 4; c += 16) tmem_st16(s_addr + h * (BK / 4) + c, pk + c);
+                tmem_wait_st();
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&bar_pready[2 * t + h]);
             }
-            l += rs;
-#pragma unroll
-            for (int c = 0; c < BK / 2; c += 16) tmem_st16(s_addr + c, pk + c);
-            tmem_wait_st();
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&bar_pready[t]);
+            l += (r2a.x + r2a.y) + (r2b.x + r2b.y);
         }
         // ------------------------------------------------------------ epilogue
         mbar_wait(&bar_ofull[t], 0);
