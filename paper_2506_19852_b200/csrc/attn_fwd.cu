@@ -28,6 +28,22 @@
 
 using namespace radial_sm100;
 
+#ifdef RADIAL_TRACE
+// Debug-only event trace (compile with -DRADIAL_TRACE): SM clock stamps for the
+// first kTraceCtas CTAs, kTraceEv events per KV step.
+__device__ unsigned long long* g_trace = nullptr;
+constexpr int kTraceCtas = 4, kTraceSteps = 64, kTraceEv = 16;
+#define TRACE(ev, j)                                                                         \
+    do {                                                                                     \
+        if (g_trace && blockIdx.x < kTraceCtas && (j) < kTraceSteps)                          \
+            g_trace[(blockIdx.x * kTraceSteps + (j)) * kTraceEv + (ev)] = clock64();         \
+    } while (0)
+#else
+#define TRACE(ev, j) \
+    do {             \
+    } while (0)
+#endif
+
 namespace {
 
 constexpr int kThreads = 384;
@@ -208,6 +224,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                         for (int h = 0; h < 2; ++h) {
                             mbar_wait(&bar_pready[2 * t + h], pphase[t]);
+                            TRACE(8 + 2 * t + h, j - 1);
                             tc_fence_after();
 #pragma unroll
                             for (int kk = h * (BK / 32); kk < (h + 1) * (BK / 32); ++kk) {
@@ -233,6 +250,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                                    sdesc_sw128(kb + off_k, 16, 1024), Cfg::kIdescS, kk ? 1u : 0u);
                         }
                         mma_commit(&bar_sfull[t]);
+                        TRACE(12 + t, j);
                         pend[t] = true;
                     }
                 }
@@ -261,7 +279,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint32_t mask = e >> 28;
             if (((mask >> (t * Cfg::GT)) & ((1u << Cfg::GT) - 1)) == 0) continue;
             const uint32_t J = e & 0x0FFFFFFFu;
+            if ((warp & 3) == 0 && lane == 0) TRACE(4 * t + 0, j);
             mbar_wait(&bar_sfull[t], sphase);
+            if ((warp & 3) == 0 && lane == 0) TRACE(4 * t + 1, j);
             sphase ^= 1;
             tc_fence_after();
             float s[BK];
@@ -357,6 +377,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&bar_pready[2 * t + h]);
+                if ((warp & 3) == 0 && lane == 0) TRACE(4 * t + 2 + h, j);
             }
             l += (r2a.x + r2a.y) + (r2b.x + r2b.y);
         }
@@ -465,6 +486,13 @@ int launch_fwd_t(const void* q, const void* k, const void* v, void* o, float* ls
     RADIAL_CUDA_TRY(cudaGetLastError());
     return RADIAL_OK;
 }
+
+#ifdef RADIAL_TRACE
+extern "C" int radial_cuda_debug_trace(void* buf) {
+    RADIAL_CUDA_TRY(cudaMemcpyToSymbol(g_trace, &buf, sizeof(void*)));
+    return RADIAL_OK;
+}
+#endif
 
 int launch_fwd(const void* q, const void* k, const void* v, void* o, float* lse, uint32_t heads,
                uint64_t n, uint32_t D, uint32_t BK, float scale, const radial_layout* L,
