@@ -112,3 +112,68 @@ extern "C" int radial_cuda_debug_tile(const void* q, const void* k, const void* 
     RADIAL_CUDA_TRY(cudaGetLastError());
     return RADIAL_OK;
 }
+
+// ---------------------------------------------------------------------------
+// MMA issue-rate microbenchmark (test/diagnostic hook): one thread per CTA
+// issues `iters` x 8 tcgen05.mma of shape 128 x N x 16 from operands already in
+// shared memory (SS: A and B K-major; TS: A from TMEM, B MN-major) and reports
+// SM clocks per MMA.  mode: 0 = SS N=128, 1 = TS N=128, 2 = SS N=256, 3 = TS N=256.
+// ---------------------------------------------------------------------------
+namespace {
+__global__ void __launch_bounds__(128, 1) mma_rate_kernel(int mode, int iters, unsigned long long* out) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                               ~static_cast<uintptr_t>(1023));
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + 96 * 1024);
+    uint32_t* slot = reinterpret_cast<uint32_t*>(bar + 1);
+    const int warp = threadIdx.x >> 5;
+    for (int i = threadIdx.x; i < 96 * 1024 / 16; i += blockDim.x)
+        reinterpret_cast<uint4*>(smem)[i] = make_uint4(0x3c003c00u, 0, 0x3c003c00u, 0);
+    if (threadIdx.x == 0) {
+        mbar_init(bar, 1);
+        fence_barrier_init();
+    }
+    if (warp == 1) tmem_alloc(slot, 512);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *slot;
+    if (threadIdx.x == 0) {
+        const uint32_t a = smem_u32(smem), b = smem_u32(smem + 32 * 1024);
+        const int N = (mode >= 2) ? 256 : 128;
+        const bool ts = mode & 1;
+        const uint32_t idesc = idesc_bf16(128, N, 0, ts ? 1 : 0);
+        const unsigned long long t0 = clock64();
+        for (int it = 0; it < iters; ++it) {
+#pragma unroll
+            for (int kk = 0; kk < 8; ++kk) {
+                if (ts)
+                    mma_ts(tmem + 256, tmem + kk * 8, sdesc_sw128(b + kk * 2048, N * 128 / 2, 1024), idesc, 1u);
+                else
+                    mma_ss(tmem, sdesc_sw128(a + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024),
+                           sdesc_sw128(b + (kk >> 2) * (N * 128) + (kk & 3) * 32, 16, 1024), idesc, 1u);
+            }
+        }
+        mma_commit(bar);
+        mbar_wait(bar, 0);
+        const unsigned long long t1 = clock64();
+        out[blockIdx.x] = (t1 - t0);
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        tmem_dealloc(tmem, 512);
+    }
+}
+}  // namespace
+
+extern "C" int radial_cuda_debug_mma_rate(int mode, int iters, int ctas, unsigned long long* out_dev) {
+    const int smem = 96 * 1024 + 64 + 1024;
+    RADIAL_CUDA_TRY(cudaFuncSetAttribute(mma_rate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    mma_rate_kernel<<<ctas, 128, smem>>>(mode, iters, out_dev);
+    RADIAL_CUDA_TRY(cudaGetLastError());
+    RADIAL_CUDA_TRY(cudaDeviceSynchronize());
+    return RADIAL_OK;
+}
