@@ -22,6 +22,7 @@
 // order (PV_t(j-1) before S_t(j)) makes that alias safe.  Online softmax in
 // the exp2 domain with lazy (threshold 8) rescaling of O in TMEM.
 #include <cmath>
+#include <type_traits>
 
 #include "radial_internal.h"
 #include "sm100.cuh"
@@ -47,11 +48,9 @@ constexpr int kTraceCtas = 4, kTraceSteps = 64, kTraceEv = 16;
 namespace {
 
 constexpr int kThreads = 384;
+constexpr uint32_t kTmem = 0;   // TMEM base address (checked against tcgen05.alloc)
 constexpr int kBQ = 128;        // query rows per tile
-#ifndef RADIAL_STAGES_K
-#define RADIAL_STAGES_K 2
-#endif
-constexpr int kStagesK = RADIAL_STAGES_K;
+constexpr int kStagesK = 2;   // the MMA loop is unrolled by the ring depth (2)
 constexpr int kStagesV = 2;
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
 #ifndef RADIAL_POLY_PAIRS
@@ -164,11 +163,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
-    const uint32_t tmem = *tmem_slot;
+    // The CTA owns all TMEM columns of its SM (one CTA per SM), so the allocation
+    // starts at lane 0 / column 0; the constant base keeps tcgen05 operands uniform.
+    if (*tmem_slot != 0) __trap();
+    constexpr uint32_t tmem = kTmem;
     // producer / MMA / allocator warpgroup needs few registers; the two softmax
-    // warpgroups hold a 128-column S row each (384 x 168 = 128 x 56 + 256 x 224)
+    // warpgroups hold a 128-column S row each (384 x 168 = 128 x 104 + 256 x 200)
     if (warp < 4) {
-        regs_dec<56>();
+        regs_dec<104>();
     if (warp == 0) {
         // ------------------------------------------------------------ producer
         if (lane == 0) {
@@ -194,75 +196,95 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
     } else if (warp == 1) {
         // ------------------------------------------------------------ MMA issuer
+        // One thread issues.  Every tcgen05 operand is (uniform smem base or the
+        // constant TMEM base) + a compile-time offset: the step loop is unrolled by
+        // the ring depth so stage indices are constants.  That keeps the operands in
+        // uniform registers; a per-MMA register->uniform move would otherwise double
+        // the issue cost of each 128x128x16 MMA (measured: 114 vs 64 clk).
         if (lane == 0) {
             mbar_wait(bar_q, 0);
             tc_fence_after();
             const uint32_t q_base = smem_u32(smem + Cfg::kSmemQ);
             const uint32_t k_base = smem_u32(smem + Cfg::kSmemK);
             const uint32_t v_base = smem_u32(smem + Cfg::kSmemV);
-            bool pend[2] = {false, false};
-            uint32_t acc[2] = {0, 0};
-            uint32_t pphase[2] = {0, 0};
-            for (uint32_t j = 0; j <= L; ++j) {
-                uint32_t tflag[2] = {0, 0};
-                const int ks = j % kStagesK;
+            bool pend0 = false, pend1 = false;
+            uint32_t acc0 = 0, acc1 = 0;
+            uint32_t pphase0 = 0, pphase1 = 0;
+            auto step = [&](uint32_t j, auto KSC) {
+                constexpr int KS = decltype(KSC)::value;  // == j % 2 (K ring and V ring)
+                constexpr int VSP = KS ^ 1;               // V stage of step j-1
+                uint32_t tf0 = 0, tf1 = 0;
                 if (j < L) {
                     const uint32_t m = entry(j) >> 28;
-                    tflag[0] = m & ((1u << Cfg::GT) - 1);
-                    tflag[1] = (m >> Cfg::GT) & ((1u << Cfg::GT) - 1);
-                    mbar_wait(&bar_kfull[ks], (j / kStagesK) & 1);
+                    tf0 = m & ((1u << Cfg::GT) - 1);
+                    tf1 = (m >> Cfg::GT) & ((1u << Cfg::GT) - 1);
+                    mbar_wait(&bar_kfull[KS], (j >> 1) & 1);
                 }
-                if (j > 0 && (pend[0] || pend[1])) {
-                    mbar_wait(&bar_vfull[(j - 1) % kStagesV], ((j - 1) / kStagesV) & 1);
-                }
+                if (j > 0 && (pend0 || pend1)) mbar_wait(&bar_vfull[VSP], ((j - 1) >> 1) & 1);
                 tc_fence_after();
-                for (int t = 0; t < 2; ++t) {
-                    if (pend[t]) {
-                        const uint32_t vb = v_base + ((j - 1) % kStagesV) * Cfg::kKVBytes;
-                        const uint32_t p_col = t ? Cfg::kColS1 : Cfg::kColS0;
-                        const uint32_t o_col = t ? Cfg::kColO1 : Cfg::kColO0;
+                auto pv = [&](auto TC, uint32_t& acc, uint32_t& pphase) {
+                    constexpr int T = decltype(TC)::value;
+                    constexpr uint32_t p_col = T ? Cfg::kColS1 : Cfg::kColS0;
+                    constexpr uint32_t o_col = T ? Cfg::kColO1 : Cfg::kColO0;
+                    const uint32_t vb = v_base + VSP * Cfg::kKVBytes;
 #pragma unroll
-                        for (int h = 0; h < 2; ++h) {
-                            mbar_wait(&bar_pready[2 * t + h], pphase[t]);
-                            TRACE(8 + 2 * t + h, j - 1);
-                            tc_fence_after();
+                    for (int h = 0; h < 2; ++h) {
+                        mbar_wait(&bar_pready[2 * T + h], pphase);
+                        TRACE(8 + 2 * T + h, j - 1);
+                        tc_fence_after();
 #pragma unroll
-                            for (int kk = h * (BK / 32); kk < (h + 1) * (BK / 32); ++kk) {
-                                const uint64_t bdesc =
-                                    sdesc_sw128(vb + kk * 16 * 128, Cfg::kKVAtomBytes, 1024);
-                                mma_ts(tmem + o_col, tmem + p_col + kk * 8, bdesc, Cfg::kIdescO,
-                                       (acc[t] | kk) ? 1u : 0u);
-                            }
-                        }
-                        pphase[t] ^= 1;
-                        acc[t] = 1;
-                        pend[t] = false;
+                        for (int kk = h * (BK / 32); kk < (h + 1) * (BK / 32); ++kk)
+                            mma_ts(kTmem + o_col, kTmem + p_col + kk * 8,
+                                   sdesc_sw128(vb + kk * 16 * 128, Cfg::kKVAtomBytes, 1024), Cfg::kIdescO,
+                                   (acc | kk) ? 1u : 0u);
                     }
-                    if (tflag[t]) {
-                        const uint32_t qb = q_base + t * Cfg::kQBytes;
-                        const uint32_t kb = k_base + ks * Cfg::kKVBytes;
-                        const uint32_t s_col = t ? Cfg::kColS1 : Cfg::kColS0;
+                    pphase ^= 1;
+                    acc = 1;
+                };
+                auto qk = [&](auto TC) {
+                    constexpr int T = decltype(TC)::value;
+                    constexpr uint32_t s_col = T ? Cfg::kColS1 : Cfg::kColS0;
+                    const uint32_t qb = q_base + T * Cfg::kQBytes;
+                    const uint32_t kb = k_base + KS * Cfg::kKVBytes;
 #pragma unroll
-                        for (int kk = 0; kk < D / 16; ++kk) {
-                            const uint32_t off_q = (kk >> 2) * Cfg::kQAtomBytes + (kk & 3) * 32;
-                            const uint32_t off_k = (kk >> 2) * Cfg::kKVAtomBytes + (kk & 3) * 32;
-                            mma_ss(tmem + s_col, sdesc_sw128(qb + off_q, 16, 1024),
-                                   sdesc_sw128(kb + off_k, 16, 1024), Cfg::kIdescS, kk ? 1u : 0u);
-                        }
-                        mma_commit(&bar_sfull[t]);
-                        TRACE(12 + t, j);
-                        pend[t] = true;
+                    for (int kk = 0; kk < D / 16; ++kk) {
+                        const uint32_t off_q = (kk >> 2) * Cfg::kQAtomBytes + (kk & 3) * 32;
+                        const uint32_t off_k = (kk >> 2) * Cfg::kKVAtomBytes + (kk & 3) * 32;
+                        mma_ss(kTmem + s_col, sdesc_sw128(qb + off_q, 16, 1024),
+                               sdesc_sw128(kb + off_k, 16, 1024), Cfg::kIdescS, kk ? 1u : 0u);
                     }
+                    mma_commit(&bar_sfull[T]);
+                    TRACE(12 + T, j);
+                };
+                if (pend0) {
+                    pv(std::integral_constant<int, 0>{}, acc0, pphase0);
+                    pend0 = false;
                 }
-                if (j > 0) mma_commit(&bar_vempty[(j - 1) % kStagesV]);
-                if (j < L) mma_commit(&bar_kempty[ks]);
+                if (tf0) {
+                    qk(std::integral_constant<int, 0>{});
+                    pend0 = true;
+                }
+                if (pend1) {
+                    pv(std::integral_constant<int, 1>{}, acc1, pphase1);
+                    pend1 = false;
+                }
+                if (tf1) {
+                    qk(std::integral_constant<int, 1>{});
+                    pend1 = true;
+                }
+                if (j > 0) mma_commit(&bar_vempty[VSP]);
+                if (j < L) mma_commit(&bar_kempty[KS]);
+            };
+            for (uint32_t j = 0; j <= L; j += 2) {
+                step(j, std::integral_constant<int, 0>{});
+                if (j + 1 <= L) step(j + 1, std::integral_constant<int, 1>{});
             }
             mma_commit(&bar_ofull[0]);
             mma_commit(&bar_ofull[1]);
         }
     }
     } else {
-        regs_inc<224>();
+        regs_inc<200>();
         // ------------------------------------------------------------ softmax
         const int t = (warp - 4) >> 2;                 // Q tile
         const int r = ((warp & 3) << 5) + lane;        // row in tile = TMEM lane
@@ -409,7 +431,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncthreads();
     if (warp == 2) {
         tc_fence_after();
-        tmem_dealloc(tmem, Cfg::kTmemCols);
+        tmem_dealloc(*tmem_slot, Cfg::kTmemCols);
     }
 }
 

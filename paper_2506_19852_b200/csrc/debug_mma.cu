@@ -120,7 +120,8 @@ extern "C" int radial_cuda_debug_tile(const void* q, const void* k, const void* 
 // SM clocks per MMA.  mode: 0 = SS N=128, 1 = TS N=128, 2 = SS N=256, 3 = TS N=256.
 // ---------------------------------------------------------------------------
 namespace {
-__global__ void __launch_bounds__(128, 1) mma_rate_kernel(int mode, int iters, unsigned long long* out) {
+template <bool TS, int N, int NACC>
+__global__ void __launch_bounds__(128, 1) mma_rate_kernel(int iters, unsigned long long* out) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                ~static_cast<uintptr_t>(1023));
@@ -138,20 +139,23 @@ __global__ void __launch_bounds__(128, 1) mma_rate_kernel(int mode, int iters, u
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
-    const uint32_t tmem = *slot;
+    // The CTA owns all 512 columns, so the allocation starts at column 0: using the
+    // constant keeps every tcgen05 operand in uniform registers (no waterfall loop).
+    if (*slot != 0) __trap();
+    constexpr uint32_t tmem = 0;
     if (threadIdx.x == 0) {
         const uint32_t a = smem_u32(smem), b = smem_u32(smem + 32 * 1024);
-        const int N = (mode >= 2) ? 256 : 128;
-        const bool ts = mode & 1;
-        const uint32_t idesc = idesc_bf16(128, N, 0, ts ? 1 : 0);
+        constexpr uint32_t idesc = idesc_bf16(128, N, 0, TS ? 1 : 0);
         const unsigned long long t0 = clock64();
         for (int it = 0; it < iters; ++it) {
 #pragma unroll
             for (int kk = 0; kk < 8; ++kk) {
-                if (ts)
-                    mma_ts(tmem + 256, tmem + kk * 8, sdesc_sw128(b + kk * 2048, N * 128 / 2, 1024), idesc, 1u);
+                constexpr uint32_t step = TS ? 128 : N;
+                const uint32_t dcol = (kk % NACC) * step;
+                if constexpr (TS)
+                    mma_ts(tmem + 256 + (dcol & 255u), tmem + kk * 8, sdesc_sw128(b + kk * 2048, N * 128 / 2, 1024), idesc, 1u);
                 else
-                    mma_ss(tmem, sdesc_sw128(a + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024),
+                    mma_ss(tmem + (dcol & 255u), sdesc_sw128(a + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024),
                            sdesc_sw128(b + (kk >> 2) * (N * 128) + (kk & 3) * 32, 16, 1024), idesc, 1u);
             }
         }
@@ -164,16 +168,31 @@ __global__ void __launch_bounds__(128, 1) mma_rate_kernel(int mode, int iters, u
     __syncthreads();
     if (warp == 1) {
         tc_fence_after();
-        tmem_dealloc(tmem, 512);
+        tmem_dealloc(*slot, 512);
     }
 }
 }  // namespace
 
-extern "C" int radial_cuda_debug_mma_rate(int mode, int iters, int ctas, unsigned long long* out_dev) {
+template <bool TS, int N, int NACC>
+int run_rate(int iters, int ctas, unsigned long long* out_dev) {
     const int smem = 96 * 1024 + 64 + 1024;
-    RADIAL_CUDA_TRY(cudaFuncSetAttribute(mma_rate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    mma_rate_kernel<<<ctas, 128, smem>>>(mode, iters, out_dev);
+    auto k = mma_rate_kernel<TS, N, NACC>;
+    RADIAL_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    k<<<ctas, 128, smem>>>(iters, out_dev);
     RADIAL_CUDA_TRY(cudaGetLastError());
     RADIAL_CUDA_TRY(cudaDeviceSynchronize());
     return RADIAL_OK;
+}
+
+// mode: bit0 TS, bit1 N=256, bit2 two accumulators
+extern "C" int radial_cuda_debug_mma_rate(int mode, int iters, int ctas, unsigned long long* out_dev) {
+    switch (mode & 7) {
+        case 0: return run_rate<false, 128, 1>(iters, ctas, out_dev);
+        case 1: return run_rate<true, 128, 1>(iters, ctas, out_dev);
+        case 2: return run_rate<false, 256, 1>(iters, ctas, out_dev);
+        case 3: return run_rate<true, 256, 1>(iters, ctas, out_dev);
+        case 4: return run_rate<false, 128, 2>(iters, ctas, out_dev);
+        case 5: return run_rate<true, 128, 2>(iters, ctas, out_dev);
+        default: return RADIAL_ERR_INVALID;
+    }
 }
