@@ -54,7 +54,7 @@ constexpr int kStagesK = 2;   // the MMA loop is unrolled by the ring depth (2)
 constexpr int kStagesV = 2;
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
 #ifndef RADIAL_POLY_PAIRS
-#define RADIAL_POLY_PAIRS 1
+#define RADIAL_POLY_PAIRS 0  // measured on B200: MUFU-only is fastest with the current pipeline
 #endif
 constexpr int kPolyPairs = RADIAL_POLY_PAIRS;  // column pairs per 4 using the polynomial exp2
 
