@@ -1,17 +1,566 @@
-// attn_bwd.cu -- K3 backward (placeholder until the tcgen05 backward lands).
+// attn_bwd.cu -- K3: backward of the block-sparse radial forward over the same
+// layout (no reference exists: the paper's LoRA length-extension path is out
+// of the reference's scope).  Gradients of attention.hpp:229-270:
+//
+//   P  = exp(S - lse),  S = scale * Q K^T on kept B x B blocks
+//   dV = P^T dO          dP = dO V^T          D = rowsum(dO o O)
+//   dS = P o (dP - D)    dQ = scale * dS K    dK = scale * dS^T Q
+//
+// Deterministic, no atomics, three launches:
+//   bwd_prep    D and lse*log2(e) per query row, padded to whole 128-row blocks
+//               (+inf lse / 0 D beyond n, so padded rows contribute exactly 0)
+//   bwd_dq      one CTA per (head, query block I) over its CSR row: S, dP on
+//               tcgen05 into TMEM, dS (bf16) written back to TMEM, dQ += dS K (TS MMA)
+//   bwd_dkdv    one CTA per (head, KV block J) over its CSC column: S^T, dP^T,
+//               then dV += P^T dO and dK += dS^T Q with P^T / dS^T in TMEM
+// Both stream the other operand in 128-row blocks split into two 64-row
+// sub-steps whose S / dP TMEM buffers alternate, so the tensor core computes
+// sub-step s+1 while warpgroup (s mod 2) does the elementwise work of s.
+// Block size 128 only (the layouts of the BASELINE backward configs).
+#include <cmath>
+#include <type_traits>
+
 #include "radial_internal.h"
+#include "sm100.cuh"
+
+using namespace radial_sm100;
+
+namespace radial_detail {
+int make_tmap_bf16_3d(CUtensorMap* m, const void* base, uint64_t n, uint32_t D, uint32_t heads,
+                      uint32_t box_rows);
+}
+
+namespace {
+
+constexpr int kThreads = 384;   // warp0 TMA, warp1 MMA, warp2 TMEM alloc, warps 4-11 elementwise
+constexpr int kBlk = 128;       // layout block = rows per resident tile
+constexpr int kSub = 64;        // streamed rows per sub-step
+constexpr uint32_t kTmem = 0;   // whole-SM TMEM allocation starts at column 0
+constexpr float kLog2e = 1.4426950408889634f;
+
+struct BwdParams {
+    __nv_bfloat16* dq;
+    __nv_bfloat16* dk;
+    __nv_bfloat16* dv;
+    const float* lse2;   // [H][Rpad] lse * log2(e), +inf padded
+    const float* dvec;   // [H][Rpad] D, 0 padded
+    const uint64_t* ptr;  // CSR (dq) or CSC (dkdv)
+    const uint32_t* idx;
+    const uint32_t* order;
+    uint64_t n, rpad;
+    uint32_t heads, R;
+    float scale, scale_log2;
+};
+
+// ---------------------------------------------------------------- preprocess
+__global__ void bwd_prep_kernel(const __nv_bfloat16* __restrict__ o, const __nv_bfloat16* __restrict__ dout,
+                                const float* __restrict__ lse, float* __restrict__ lse2,
+                                float* __restrict__ dvec, uint64_t n, uint64_t rpad, uint32_t D,
+                                uint32_t heads) {
+    // one warp per padded row
+    const uint64_t w = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (w >= static_cast<uint64_t>(heads) * rpad) return;
+    const uint64_t h = w / rpad, i = w % rpad;
+    float acc = 0.f;
+    if (i < n) {
+        const __nv_bfloat16* orow = o + (h * n + i) * D;
+        const __nv_bfloat16* drow = dout + (h * n + i) * D;
+        for (uint32_t c = lane * 2; c < D; c += 64) {
+            const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(orow + c));
+            const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(drow + c));
+            acc += a.x * b.x + a.y * b.y;
+        }
+    }
+    for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+    if (lane == 0) {
+        dvec[w] = i < n ? acc : 0.f;
+        lse2[w] = i < n ? lse[h * n + i] * kLog2e : INFINITY;
+    }
+}
+
+template <int D>
+struct BwdCfg {
+    static constexpr int kAtoms = D / 64;
+    static constexpr int kAtomBytes = kBlk * 128;      // 128 rows x 128 B
+    static constexpr int kTileBytes = kBlk * D * 2;    // one 128-row bf16 tile
+    static constexpr uint32_t kIdS = idesc_bf16(128, kSub, 0, 0);  // 128 x 64 x 16, K-major both
+    static constexpr uint32_t kIdAcc = idesc_bf16(128, D, 0, 1);   // 128 x D x 16, B MN-major
+};
+
+// K-major descriptor of MMA k-step kk (16 elements of d) for a 128-row tile,
+// optionally starting at row `row0` (multiple of 8).
+__device__ __forceinline__ uint64_t kdesc(uint32_t tile, int kk, int row0) {
+    return sdesc_sw128(tile + (kk >> 2) * (kBlk * 128) + row0 * 128 + (kk & 3) * 32, 16, 1024);
+}
+// MN-major descriptor (B operand with N = d) of 16 rows starting at `row0`.
+__device__ __forceinline__ uint64_t mndesc(uint32_t tile, int row0) {
+    return sdesc_sw128(tile + row0 * 128, kBlk * 128, 1024);
+}
+
+// ============================================================================ dQ
+// TMEM: S0 [0,64) S1 [64,128) dP0 [128,192) dP1 [192,256) dQ [256,256+D)
+template <int D>
+__global__ void __launch_bounds__(kThreads, 1)
+    radial_attn_bwd_dq_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_do,
+                              const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
+                              const BwdParams p) {
+    using Cfg = BwdCfg<D>;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                               ~static_cast<uintptr_t>(1023));
+    constexpr int T = Cfg::kTileBytes;
+    // [Q | dO | K0 V0 | K1 V1]
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 6 * T);
+    uint64_t* bar_res = bars;          // Q, dO landed
+    uint64_t* bar_full = bars + 1;     // [2] K/V stage landed
+    uint64_t* bar_empty = bars + 3;    // [2] K/V stage free
+    uint64_t* bar_s = bars + 5;        // [2] S/dP sub-buffer computed
+    uint64_t* bar_ds = bars + 7;       // [2] dS sub-buffer written
+    uint64_t* bar_acc = bars + 9;      // dQ final
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 10);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t head = blockIdx.x / p.R;
+    const uint32_t I = p.order[blockIdx.x % p.R];
+    const uint64_t e0 = p.ptr[I];
+    const uint32_t L = static_cast<uint32_t>(p.ptr[I + 1] - e0);
+
+    if (warp == 0 && lane == 0) {
+        mbar_init(bar_res, 1);
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&bar_full[i], 1);
+            mbar_init(&bar_empty[i], 1);
+            mbar_init(&bar_s[i], 1);
+            mbar_init(&bar_ds[i], 4);
+        }
+        mbar_init(bar_acc, 1);
+        fence_barrier_init();
+    }
+    if (warp == 2) tmem_alloc(tmem_slot, 512);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    if (*tmem_slot != 0) __trap();
+
+    if (warp < 4) {
+        regs_dec<104>();
+        if (warp == 0 && lane == 0) {
+            // ------------------------------------------------ producer
+            mbar_arrive_expect_tx(bar_res, 2 * T);
+            for (int a = 0; a < Cfg::kAtoms; ++a) {
+                tma_load_3d(smem + a * Cfg::kAtomBytes, &tm_q, bar_res, a * 64, I * kBlk, head);
+                tma_load_3d(smem + T + a * Cfg::kAtomBytes, &tm_do, bar_res, a * 64, I * kBlk, head);
+            }
+            for (uint32_t j = 0; j < L; ++j) {
+                const int st = j & 1;
+                const int32_t J = static_cast<int32_t>(__ldg(p.idx + e0 + j));
+                mbar_wait(&bar_empty[st], ((j >> 1) & 1) ^ 1);
+                mbar_arrive_expect_tx(&bar_full[st], 2 * T);
+                uint8_t* kd = smem + (2 + 2 * st) * T;
+                for (int a = 0; a < Cfg::kAtoms; ++a) {
+                    tma_load_3d(kd + a * Cfg::kAtomBytes, &tm_k, &bar_full[st], a * 64, J * kBlk, head);
+                    tma_load_3d(kd + T + a * Cfg::kAtomBytes, &tm_v, &bar_full[st], a * 64, J * kBlk, head);
+                }
+            }
+        } else if (warp == 1 && lane == 0) {
+            // ------------------------------------------------ MMA issuer
+            mbar_wait(bar_res, 0);
+            tc_fence_after();
+            const uint32_t q_s = smem_u32(smem), do_s = smem_u32(smem + T);
+            const uint32_t kv0 = smem_u32(smem + 2 * T);
+            uint32_t dsph[2] = {0, 0};
+            bool acc = false;
+            // dQ += dS(sub-buffer b) . K(rows of that sub-step)
+            auto dq_mma = [&](auto BC, uint32_t k_tile) {
+                constexpr int b = decltype(BC)::value;
+                mbar_wait(&bar_ds[b], dsph[b]);
+                dsph[b] ^= 1;
+                tc_fence_after();
+#pragma unroll
+                for (int kk = 0; kk < kSub / 16; ++kk)
+                    mma_ts(kTmem + 256, kTmem + b * 64 + kk * 8, mndesc(k_tile, b * kSub + kk * 16),
+                           Cfg::kIdAcc, (acc || kk) ? 1u : 0u);
+                acc = true;
+            };
+            for (uint32_t j = 0; j < L; ++j) {
+                const int st = j & 1;
+                const uint32_t k_s = kv0 + st * 2 * T, v_s = k_s + T;
+                const uint32_t k_prev = kv0 + (st ^ 1) * 2 * T;
+                mbar_wait(&bar_full[st], (j >> 1) & 1);
+                tc_fence_after();
+                auto sub = [&](auto BC) {
+                    constexpr int b = decltype(BC)::value;
+                    // S_b = Q K_sub^T ; dP_b = dO V_sub^T   (128 x 64, K = d)
+#pragma unroll
+                    for (int kk = 0; kk < D / 16; ++kk)
+                        mma_ss(kTmem + b * 64, kdesc(q_s, kk, 0), kdesc(k_s, kk, b * kSub), Cfg::kIdS, kk ? 1u : 0u);
+#pragma unroll
+                    for (int kk = 0; kk < D / 16; ++kk)
+                        mma_ss(kTmem + 128 + b * 64, kdesc(do_s, kk, 0), kdesc(v_s, kk, b * kSub), Cfg::kIdS,
+                               kk ? 1u : 0u);
+                    mma_commit(&bar_s[b]);
+                };
+                sub(std::integral_constant<int, 0>{});
+                if (j > 0) {  // previous block's second sub-step, then free its K/V stage
+                    dq_mma(std::integral_constant<int, 1>{}, k_prev);
+                    mma_commit(&bar_empty[st ^ 1]);
+                }
+                sub(std::integral_constant<int, 1>{});
+                dq_mma(std::integral_constant<int, 0>{}, k_s);
+            }
+            if (L > 0) dq_mma(std::integral_constant<int, 1>{}, kv0 + ((L - 1) & 1) * 2 * T);
+            mma_commit(bar_acc);
+        }
+    } else {
+        regs_inc<200>();
+        // ---------------------------------------------------- elementwise
+        const int wg = (warp - 4) >> 2;  // sub-buffer this warpgroup owns
+        const int r = ((warp & 3) << 5) + lane;
+        const uint32_t la = static_cast<uint32_t>((warp & 3) * 32) << 16;
+        const uint64_t row = static_cast<uint64_t>(I) * kBlk + r;
+        const uint64_t prow = static_cast<uint64_t>(head) * p.rpad + row;
+        const float lse2 = p.lse2[prow];
+        const float dval = p.dvec[prow];
+        const float sl2 = p.scale_log2;
+        for (uint32_t j = 0; j < L; ++j) {
+            const uint32_t J = __ldg(p.idx + e0 + j);
+            mbar_wait(&bar_s[wg], j & 1);
+            tc_fence_after();
+            uint32_t sv[64], dp[64];
+            tmem_ld32(kTmem + la + wg * 64, *reinterpret_cast<uint32_t(*)[32]>(sv));
+            tmem_ld32(kTmem + la + wg * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(sv + 32));
+            tmem_ld32(kTmem + la + 128 + wg * 64, *reinterpret_cast<uint32_t(*)[32]>(dp));
+            tmem_ld32(kTmem + la + 128 + wg * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(dp + 32));
+            tmem_wait_ld();
+            const uint64_t key0 = static_cast<uint64_t>(J) * kBlk + wg * kSub;
+            const int valid = key0 + kSub <= p.n ? kSub : (key0 < p.n ? static_cast<int>(p.n - key0) : 0);
+            uint32_t pk[32];
+#pragma unroll
+            for (int c = 0; c < kSub; c += 2) {
+                float p0 = ex2(fmaf(__uint_as_float(sv[c]), sl2, -lse2));
+                float p1 = ex2(fmaf(__uint_as_float(sv[c + 1]), sl2, -lse2));
+                if (valid < kSub) {
+                    p0 = c < valid ? p0 : 0.f;
+                    p1 = c + 1 < valid ? p1 : 0.f;
+                }
+                const float d0 = p0 * (__uint_as_float(dp[c]) - dval);
+                const float d1 = p1 * (__uint_as_float(dp[c + 1]) - dval);
+                pk[c / 2] = pack_bf16(d0, d1);
+            }
+            tmem_st16(kTmem + la + wg * 64, pk);
+            tmem_st16(kTmem + la + wg * 64 + 16, pk + 16);
+            tmem_wait_st();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&bar_ds[wg]);
+        }
+        // ---------------------------------------------------- epilogue: dQ * scale
+        mbar_wait(bar_acc, 0);
+        tc_fence_after();
+        constexpr int kHalf = D / 2;
+#pragma unroll
+        for (int c = 0; c < kHalf; c += 32) {
+            uint32_t u[32];
+            tmem_ld32(kTmem + la + 256 + wg * kHalf + c, u);
+            tmem_wait_ld();
+            if (row < p.n) {
+                uint32_t w[16];
+#pragma unroll
+                for (int x = 0; x < 16; ++x)
+                    w[x] = pack_bf16(__uint_as_float(u[2 * x]) * p.scale, __uint_as_float(u[2 * x + 1]) * p.scale);
+                uint4* dst = reinterpret_cast<uint4*>(p.dq + (static_cast<uint64_t>(head) * p.n + row) * D + wg * kHalf + c);
+#pragma unroll
+                for (int x = 0; x < 4; ++x) dst[x] = make_uint4(w[4 * x], w[4 * x + 1], w[4 * x + 2], w[4 * x + 3]);
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 2) {
+        tc_fence_after();
+        tmem_dealloc(*tmem_slot, 512);
+    }
+}
+
+// ========================================================================== dK/dV
+// TMEM: S^T0 [0,64) S^T1 [64,128) dP^T0 [128,192) dP^T1 [192,256) dV [256,256+D) dK [256+D, 256+2D)
+// P^T (bf16) overwrites S^T_b columns [b*64, b*64+32); dS^T overwrites dP^T_b [128+b*64, +32).
+template <int D>
+__global__ void __launch_bounds__(kThreads, 1)
+    radial_attn_bwd_dkdv_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_do,
+                                const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
+                                const BwdParams p) {
+    using Cfg = BwdCfg<D>;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                               ~static_cast<uintptr_t>(1023));
+    constexpr int T = Cfg::kTileBytes;
+    // [K | V | Q0 dO0 | Q1 dO1 | lse2/D stage0 (1 KB) | stage1 (1 KB)]
+    float* vec = reinterpret_cast<float*>(smem + 6 * T);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 6 * T + 2048);
+    uint64_t* bar_res = bars;
+    uint64_t* bar_full = bars + 1;
+    uint64_t* bar_empty = bars + 3;
+    uint64_t* bar_s = bars + 5;
+    uint64_t* bar_p = bars + 7;
+    uint64_t* bar_acc = bars + 9;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 10);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t head = blockIdx.x / p.R;
+    const uint32_t J = p.order[blockIdx.x % p.R];
+    const uint64_t e0 = p.ptr[J];
+    const uint32_t L = static_cast<uint32_t>(p.ptr[J + 1] - e0);
+
+    if (warp == 0 && lane == 0) {
+        mbar_init(bar_res, 1);
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&bar_full[i], 1);
+            mbar_init(&bar_empty[i], 1);
+            mbar_init(&bar_s[i], 1);
+            mbar_init(&bar_p[i], 4);
+        }
+        mbar_init(bar_acc, 1);
+        fence_barrier_init();
+    }
+    if (warp == 2) tmem_alloc(tmem_slot, 512);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    if (*tmem_slot != 0) __trap();
+
+    if (warp < 4) {
+        regs_dec<104>();
+        if (warp == 0 && lane == 0) {
+            mbar_arrive_expect_tx(bar_res, 2 * T);
+            for (int a = 0; a < Cfg::kAtoms; ++a) {
+                tma_load_3d(smem + a * Cfg::kAtomBytes, &tm_k, bar_res, a * 64, J * kBlk, head);
+                tma_load_3d(smem + T + a * Cfg::kAtomBytes, &tm_v, bar_res, a * 64, J * kBlk, head);
+            }
+            for (uint32_t j = 0; j < L; ++j) {
+                const int st = j & 1;
+                const uint32_t Iq = __ldg(p.idx + e0 + j);
+                mbar_wait(&bar_empty[st], ((j >> 1) & 1) ^ 1);
+                mbar_arrive_expect_tx(&bar_full[st], 2 * T + 2 * kBlk * 4);
+                uint8_t* qd = smem + (2 + 2 * st) * T;
+                for (int a = 0; a < Cfg::kAtoms; ++a) {
+                    tma_load_3d(qd + a * Cfg::kAtomBytes, &tm_q, &bar_full[st], a * 64, Iq * kBlk, head);
+                    tma_load_3d(qd + T + a * Cfg::kAtomBytes, &tm_do, &bar_full[st], a * 64, Iq * kBlk, head);
+                }
+                const uint64_t off = static_cast<uint64_t>(head) * p.rpad + static_cast<uint64_t>(Iq) * kBlk;
+                bulk_load(vec + st * 256, p.lse2 + off, kBlk * 4, &bar_full[st]);
+                bulk_load(vec + st * 256 + 128, p.dvec + off, kBlk * 4, &bar_full[st]);
+            }
+        } else if (warp == 1 && lane == 0) {
+            mbar_wait(bar_res, 0);
+            tc_fence_after();
+            const uint32_t k_s = smem_u32(smem), v_s = smem_u32(smem + T);
+            const uint32_t qd0 = smem_u32(smem + 2 * T);
+            uint32_t pph[2] = {0, 0};
+            bool acc = false;
+            // dV += P^T_b dO_sub ; dK += dS^T_b Q_sub   (K = 64 streamed rows)
+            auto acc_mma = [&](auto BC, uint32_t q_tile) {
+                constexpr int b = decltype(BC)::value;
+                mbar_wait(&bar_p[b], pph[b]);
+                pph[b] ^= 1;
+                tc_fence_after();
+                const uint32_t do_tile = q_tile + T;
+#pragma unroll
+                for (int kk = 0; kk < kSub / 16; ++kk)
+                    mma_ts(kTmem + 256, kTmem + b * 64 + kk * 8, mndesc(do_tile, b * kSub + kk * 16), Cfg::kIdAcc,
+                           (acc || kk) ? 1u : 0u);
+#pragma unroll
+                for (int kk = 0; kk < kSub / 16; ++kk)
+                    mma_ts(kTmem + 256 + D, kTmem + 128 + b * 64 + kk * 8, mndesc(q_tile, b * kSub + kk * 16),
+                           Cfg::kIdAcc, (acc || kk) ? 1u : 0u);
+                acc = true;
+            };
+            for (uint32_t j = 0; j < L; ++j) {
+                const int st = j & 1;
+                const uint32_t q_t = qd0 + st * 2 * T, do_t = q_t + T;
+                const uint32_t q_prev = qd0 + (st ^ 1) * 2 * T;
+                mbar_wait(&bar_full[st], (j >> 1) & 1);
+                tc_fence_after();
+                auto sub = [&](auto BC) {
+                    constexpr int b = decltype(BC)::value;
+                    // S^T_b = K Q_sub^T ; dP^T_b = V dO_sub^T   (128 keys x 64 queries, K = d)
+#pragma unroll
+                    for (int kk = 0; kk < D / 16; ++kk)
+                        mma_ss(kTmem + b * 64, kdesc(k_s, kk, 0), kdesc(q_t, kk, b * kSub), Cfg::kIdS, kk ? 1u : 0u);
+#pragma unroll
+                    for (int kk = 0; kk < D / 16; ++kk)
+                        mma_ss(kTmem + 128 + b * 64, kdesc(v_s, kk, 0), kdesc(do_t, kk, b * kSub), Cfg::kIdS,
+                               kk ? 1u : 0u);
+                    mma_commit(&bar_s[b]);
+                };
+                sub(std::integral_constant<int, 0>{});
+                if (j > 0) {
+                    acc_mma(std::integral_constant<int, 1>{}, q_prev);
+                    mma_commit(&bar_empty[st ^ 1]);
+                }
+                sub(std::integral_constant<int, 1>{});
+                acc_mma(std::integral_constant<int, 0>{}, q_t);
+            }
+            if (L > 0) acc_mma(std::integral_constant<int, 1>{}, qd0 + ((L - 1) & 1) * 2 * T);
+            mma_commit(bar_acc);
+        }
+    } else {
+        regs_inc<200>();
+        const int wg = (warp - 4) >> 2;
+        const int r = ((warp & 3) << 5) + lane;  // key row of the tile
+        const uint32_t la = static_cast<uint32_t>((warp & 3) * 32) << 16;
+        const uint64_t krow = static_cast<uint64_t>(J) * kBlk + r;
+        const float sl2 = p.scale_log2;
+        for (uint32_t j = 0; j < L; ++j) {
+            const int st = j & 1;
+            mbar_wait(&bar_s[wg], j & 1);
+            tc_fence_after();
+            uint32_t sv[64], dp[64];
+            tmem_ld32(kTmem + la + wg * 64, *reinterpret_cast<uint32_t(*)[32]>(sv));
+            tmem_ld32(kTmem + la + wg * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(sv + 32));
+            tmem_ld32(kTmem + la + 128 + wg * 64, *reinterpret_cast<uint32_t(*)[32]>(dp));
+            tmem_ld32(kTmem + la + 128 + wg * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(dp + 32));
+            tmem_wait_ld();
+            // lse2 / D of the 64 query columns (already landed with this stage's Q/dO)
+            const float4* lv = reinterpret_cast<const float4*>(vec + st * 256 + wg * kSub);
+            const float4* dvv = reinterpret_cast<const float4*>(vec + st * 256 + 128 + wg * kSub);
+            uint32_t pp[32], pd[32];
+#pragma unroll
+            for (int c4 = 0; c4 < kSub / 4; ++c4) {
+                const float4 l4 = lv[c4], d4 = dvv[c4];
+                const float ls[4] = {l4.x, l4.y, l4.z, l4.w};
+                const float ds_[4] = {d4.x, d4.y, d4.z, d4.w};
+                float pv[4], dv[4];
+#pragma unroll
+                for (int x = 0; x < 4; ++x) {
+                    const int c = c4 * 4 + x;
+                    pv[x] = ex2(fmaf(__uint_as_float(sv[c]), sl2, -ls[x]));
+                    dv[x] = pv[x] * (__uint_as_float(dp[c]) - ds_[x]);
+                }
+                pp[c4 * 2] = pack_bf16(pv[0], pv[1]);
+                pp[c4 * 2 + 1] = pack_bf16(pv[2], pv[3]);
+                pd[c4 * 2] = pack_bf16(dv[0], dv[1]);
+                pd[c4 * 2 + 1] = pack_bf16(dv[2], dv[3]);
+            }
+            tmem_st16(kTmem + la + wg * 64, pp);
+            tmem_st16(kTmem + la + wg * 64 + 16, pp + 16);
+            tmem_st16(kTmem + la + 128 + wg * 64, pd);
+            tmem_st16(kTmem + la + 128 + wg * 64 + 16, pd + 16);
+            tmem_wait_st();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&bar_p[wg]);
+        }
+        // ---------------------------------------------------- epilogue: wg0 -> dV, wg1 -> dK * scale
+        mbar_wait(bar_acc, 0);
+        tc_fence_after();
+        const float mul = wg ? p.scale : 1.f;
+        __nv_bfloat16* out = (wg ? p.dk : p.dv) + (static_cast<uint64_t>(head) * p.n + krow) * D;
+#pragma unroll
+        for (int c = 0; c < D; c += 32) {
+            uint32_t u[32];
+            tmem_ld32(kTmem + la + 256 + wg * D + c, u);
+            tmem_wait_ld();
+            if (krow < p.n) {
+                uint32_t w[16];
+#pragma unroll
+                for (int x = 0; x < 16; ++x)
+                    w[x] = pack_bf16(__uint_as_float(u[2 * x]) * mul, __uint_as_float(u[2 * x + 1]) * mul);
+                uint4* dst = reinterpret_cast<uint4*>(out + c);
+#pragma unroll
+                for (int x = 0; x < 4; ++x) dst[x] = make_uint4(w[4 * x], w[4 * x + 1], w[4 * x + 2], w[4 * x + 3]);
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 2) {
+        tc_fence_after();
+        tmem_dealloc(*tmem_slot, 512);
+    }
+}
+
+template <int D>
+int launch_bwd_t(const void* q, const void* k, const void* v, const void* o, const float* lse,
+                 const void* dout, void* dq, void* dk, void* dv, uint32_t heads, uint64_t n,
+                 float scale, const radial_layout* L, void* workspace, cudaStream_t st) {
+    using namespace radial_detail;
+    const uint64_t R = L->R;
+    const uint64_t rpad = R * kBlk;
+    float* lse2 = static_cast<float*>(workspace);
+    float* dvec = lse2 + heads * rpad;
+    {
+        const uint64_t warps = heads * rpad;
+        const unsigned blocks = static_cast<unsigned>((warps * 32 + 255) / 256);
+        bwd_prep_kernel<<<blocks, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(o),
+                                                 static_cast<const __nv_bfloat16*>(dout), lse, lse2, dvec, n,
+                                                 rpad, D, heads);
+        RADIAL_CUDA_TRY(cudaGetLastError());
+    }
+    CUtensorMap tq, tdo, tk, tv;
+    int rc;
+    if ((rc = make_tmap_bf16_3d(&tq, q, n, D, heads, kBlk))) return rc;
+    if ((rc = make_tmap_bf16_3d(&tdo, dout, n, D, heads, kBlk))) return rc;
+    if ((rc = make_tmap_bf16_3d(&tk, k, n, D, heads, kBlk))) return rc;
+    if ((rc = make_tmap_bf16_3d(&tv, v, n, D, heads, kBlk))) return rc;
+    BwdParams p{};
+    p.dq = static_cast<__nv_bfloat16*>(dq);
+    p.dk = static_cast<__nv_bfloat16*>(dk);
+    p.dv = static_cast<__nv_bfloat16*>(dv);
+    p.lse2 = lse2;
+    p.dvec = dvec;
+    p.n = n;
+    p.rpad = rpad;
+    p.heads = heads;
+    p.R = static_cast<uint32_t>(R);
+    p.scale = scale;
+    p.scale_log2 = scale * kLog2e;
+    const uint64_t items = heads * R;
+    if (items > 0x7fffffffull) return fail(RADIAL_ERR_INVALID, "attn_bwd: too many work items");
+    const int T = BwdCfg<D>::kTileBytes;
+    {
+        const int smem = 6 * T + 128 + 1024;
+        auto kern = radial_attn_bwd_dq_kernel<D>;
+        RADIAL_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        p.ptr = L->row_ptr;
+        p.idx = L->col_idx;
+        p.order = L->rorder;
+        kern<<<static_cast<unsigned>(items), kThreads, smem, st>>>(tq, tdo, tk, tv, p);
+        RADIAL_CUDA_TRY(cudaGetLastError());
+    }
+    {
+        const int smem = 6 * T + 2048 + 128 + 1024;
+        auto kern = radial_attn_bwd_dkdv_kernel<D>;
+        RADIAL_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        p.ptr = L->col_ptr;
+        p.idx = L->row_idx;
+        p.order = L->corder;
+        kern<<<static_cast<unsigned>(items), kThreads, smem, st>>>(tq, tdo, tk, tv, p);
+        RADIAL_CUDA_TRY(cudaGetLastError());
+    }
+    return RADIAL_OK;
+}
+
+}  // namespace
 
 namespace radial_detail {
 
 size_t bwd_workspace_bytes(uint32_t heads, uint64_t n, uint32_t D) {
     (void)D;
-    return static_cast<size_t>(heads) * n * sizeof(float) + 256;
+    const uint64_t rpad = ((n + kBlk - 1) / kBlk) * kBlk;
+    return static_cast<size_t>(2) * heads * rpad * sizeof(float) + 256;
 }
 
-int launch_bwd(const void*, const void*, const void*, const void*, const float*, const void*, void*,
-               void*, void*, uint32_t, uint64_t, uint32_t, float, const radial_layout*, void*,
-               cudaStream_t) {
-    return fail(RADIAL_ERR_INVALID, "attn_bwd: not built in this version");
+int launch_bwd(const void* q, const void* k, const void* v, const void* o, const float* lse,
+               const void* dout, void* dq, void* dk, void* dv, uint32_t heads, uint64_t n, uint32_t D,
+               float scale, const radial_layout* L, void* workspace, cudaStream_t st) {
+    if (!workspace) return fail(RADIAL_ERR_INVALID, "attn_bwd: null workspace");
+    if (L->B != kBlk) return fail(RADIAL_ERR_INVALID, "attn_bwd: block_size must be 128 on the device path");
+    if (!L->rorder || !L->corder) return fail(RADIAL_ERR_INVALID, "attn_bwd: layout has no work lists");
+    if (D == 128) return launch_bwd_t<128>(q, k, v, o, lse, dout, dq, dk, dv, heads, n, scale, L, workspace, st);
+    if (D == 64) return launch_bwd_t<64>(q, k, v, o, lse, dout, dq, dk, dv, heads, n, scale, L, workspace, st);
+    return fail(RADIAL_ERR_INVALID, "attn_bwd: head_dim must be 64 or 128");
 }
 
 }  // namespace radial_detail

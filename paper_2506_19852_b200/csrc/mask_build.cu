@@ -341,6 +341,10 @@ int build_worklists(radial_layout* L, cudaStream_t st) {
     if (rc) return rc;
     if (hs.nnz != L->nnz) return fail(RADIAL_ERR_INVALID, "layout transpose size mismatch");
     if (L->B != 64 && L->B != 128) return RADIAL_OK;  // attention kernels not instantiated
+    rc = lpt_order(L->row_ptr, L->R, st, &L->rorder);
+    if (rc) return rc;
+    rc = lpt_order(L->col_ptr, L->R, st, &L->corder);
+    if (rc) return rc;
     L->G = 256 / L->B;
     L->C = (L->R + L->G - 1) / L->G;
     rc = build_lists(ChunkUnion{L->row_ptr, L->col_idx, L->R, L->G}, L->C, L->R, 1, st, &L->uptr,

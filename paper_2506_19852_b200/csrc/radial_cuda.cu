@@ -38,8 +38,8 @@ namespace {
 
 void free_layout(radial_layout* L) {
     if (!L) return;
-    void* ptrs[] = {L->row_ptr, L->col_idx, L->col_ptr, L->row_idx, L->uptr,
-                    L->uidx,    L->uorder,  L->tptr,    L->tidx,    L->torder};
+    void* ptrs[] = {L->row_ptr, L->col_idx, L->col_ptr, L->row_idx, L->uptr,   L->uidx,
+                    L->uorder,  L->tptr,    L->tidx,    L->torder,  L->rorder, L->corder};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     delete L;

@@ -36,6 +36,9 @@ struct radial_layout {
     uint64_t* tptr = nullptr;
     uint32_t* tidx = nullptr;
     uint32_t* torder = nullptr;
+    // Backward per-block orders (longest list first): CSR rows (dQ), CSC columns (dK/dV)
+    uint32_t* rorder = nullptr;
+    uint32_t* corder = nullptr;
 };
 
 namespace radial_detail {

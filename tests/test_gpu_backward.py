@@ -1,0 +1,148 @@
+"""GPU parity: K3 backward (dQ, dK, dV over the block layout) against the fp64 oracle
+(oracle.attention_bwd, cross-checked against torch autograd in tests/test_oracle.py) and,
+at the full Mochi-1 shape, against a torch fp32 restatement on sampled blocks.
+
+No reference backward exists; the bar is the bf16 training tolerance below,
+evaluated per (head, block)."""
+import numpy as np
+import pytest
+
+import oracle as O
+from tests._util import instance_bf16, to_torch_bf16
+
+pytestmark = pytest.mark.gpu
+
+BWD_REL_L2 = 2e-2   # per block; bf16 P/dS operands with fp32 accumulation
+BWD_GLOBAL = 1e-2   # whole tensor
+
+
+@pytest.fixture(scope="module")
+def P():
+    import torch
+    assert torch.cuda.is_available(), "GPU test on a box without CUDA"
+    import paper_2506_19852_b200 as P
+    return P
+
+
+def _rel(a, b):
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-30))
+
+
+def _check_blocks(got, want, B, what):
+    n = want.shape[0]
+    worst = 0.0
+    for I in range((n + B - 1) // B):
+        sl = slice(I * B, min(n, (I + 1) * B))
+        worst = max(worst, _rel(got[sl].astype(np.float64), want[sl]))
+    glob = _rel(got.astype(np.float64), want)
+    assert worst <= BWD_REL_L2 and glob <= BWD_GLOBAL, f"{what}: per-block rel-L2 {worst:.3e}, global {glob:.3e}"
+    return worst, glob
+
+
+@pytest.mark.parametrize("f,s,d,sink", [(4, 300, 128, True), (3, 257, 64, True), (6, 200, 128, False),
+                                        (2, 64, 128, True), (5, 333, 64, False)])
+def test_backward_vs_fp64_oracle(P, f, s, d, sink):
+    import torch
+    H, B = 2, 128
+    n = f * s
+    q, k, v = instance_bf16(f, s, d, H, 17)
+    dout = np.stack([O.bf16_round(O.random_instance(n, d, 900 + h)[0]) for h in range(H)])
+    lay = P.device_layout(P.GridShape(f, s), P.PatternSpec.radial(sink), B)
+    tq, tk, tv, tdo = (to_torch_bf16(x) for x in (q, k, v, dout))
+    o, lse = P.masked_attention(tq, tk, tv, lay, return_lse=True)
+    dq, dk, dv = P.masked_attention_backward(tq, tk, tv, o, lse, tdo, lay)
+    torch.cuda.synchronize()
+    host = lay.host()
+    for h in range(H):
+        wq, wk, wv = O.attention_bwd(q[h], k[h], v[h], dout[h], B, host.row_ptr, host.col_idx)
+        _check_blocks(dq[h].float().cpu().numpy(), wq, B, f"dQ head {h}")
+        _check_blocks(dk[h].float().cpu().numpy(), wk, B, f"dK head {h}")
+        _check_blocks(dv[h].float().cpu().numpy(), wv, B, f"dV head {h}")
+
+
+def test_backward_matches_torch_autograd_dense_mask(P):
+    """torch fp32 autograd of softmax(QK^T/sqrt(d) + block mask) V on the same bf16 inputs."""
+    import torch
+    f, s, d, H, B = 8, 256, 128, 2, 128
+    n = f * s
+    g = torch.Generator(device="cuda").manual_seed(5)
+    q, k, v, do = (torch.randn(H, n, d, device="cuda", generator=g).to(torch.bfloat16) for _ in range(4))
+    lay = P.device_layout(P.GridShape(f, s), P.PatternSpec.radial(), B)
+    o, lse = P.masked_attention(q, k, v, lay, return_lse=True)
+    dq, dk, dv = P.masked_attention_backward(q, k, v, o, lse, do, lay)
+    host = lay.host()
+    R = host.grid_rows
+    mask = torch.zeros(n, n, dtype=torch.bool, device="cuda")
+    for I in range(R):
+        for J in host.col_idx[host.row_ptr[I]:host.row_ptr[I + 1]]:
+            mask[I * B:(I + 1) * B, int(J) * B:(int(J) + 1) * B] = True
+    qf, kf, vf = (x.float().requires_grad_(True) for x in (q, k, v))
+    sc = (qf @ kf.transpose(1, 2)) / d ** 0.5
+    sc = sc.masked_fill(~mask, float("-inf"))
+    of = torch.softmax(sc, -1) @ vf
+    of.backward(do.float())
+    for name, got, ref in (("dq", dq, qf.grad), ("dk", dk, kf.grad), ("dv", dv, vf.grad)):
+        rel = ((got.float() - ref).norm() / ref.norm()).item()
+        assert rel < BWD_GLOBAL, f"{name} rel-L2 {rel:.3e}"
+    rel_o = ((o.float() - of.detach()).norm() / of.norm()).item()
+    assert rel_o < 1e-2
+
+
+def test_backward_mochi28_full_shape_sampled(P):
+    """BASELINE configs[3] (Mochi-1 28 x 1590, 24 heads, d 128) at full size: all heads on
+    the GPU; sampled query blocks (dQ) and KV blocks (dK, dV) -- sink column, tail, random --
+    against a torch fp32 restatement of the gradients over exactly the kept blocks."""
+    import torch
+    f, s, d, H, B = 28, 1590, 128, 24, 128
+    n = f * s
+    g = torch.Generator(device="cuda").manual_seed(11)
+    q, k, v, do = (torch.randn(H, n, d, device="cuda", generator=g).to(torch.bfloat16) for _ in range(4))
+    lay = P.device_layout(P.GridShape(f, s), P.PatternSpec.radial(), B)
+    o, lse = P.masked_attention(q, k, v, lay, return_lse=True)
+    dq, dk, dv = P.masked_attention_backward(q, k, v, o, lse, do, lay)
+    torch.cuda.synchronize()
+    host = lay.host()
+    cp, ri = lay.csc()
+    R = host.grid_rows
+    scale = d ** -0.5
+
+    def rows_of(I):
+        return torch.arange(I * B, min(n, (I + 1) * B), device="cuda")
+
+    def keys_of(lst):
+        return torch.cat([rows_of(int(J)) for J in lst])
+
+    for h in (0, 17):
+        qf, kf, vf, dof = (x[h].float() for x in (q, k, v, do))
+        # fp32 row statistics (lse, D) for any query block, restated from the forward
+        def stats(I):
+            rr = rows_of(I)
+            kk = keys_of(host.col_idx[host.row_ptr[I]:host.row_ptr[I + 1]])
+            sc = (qf[rr] @ kf[kk].T) * scale
+            lse_r = torch.logsumexp(sc, -1)
+            p = torch.exp(sc - lse_r[:, None])
+            o_r = p @ vf[kk]
+            return rr, kk, p, (dof[rr] * o_r).sum(-1)
+
+        for I in (0, R // 2, R - 1):
+            rr, kk, p, Dr = stats(I)
+            dp = dof[rr] @ vf[kk].T
+            ds = p * (dp - Dr[:, None])
+            want = (ds @ kf[kk]) * scale
+            rel = ((dq[h, rr].float() - want).norm() / want.norm()).item()
+            assert rel < BWD_REL_L2, f"dQ head {h} block {I}: {rel:.3e}"
+        for J in (0, 1, R // 3, R - 1):
+            kk = rows_of(J)
+            dk_w = torch.zeros(len(kk), d, device="cuda")
+            dv_w = torch.zeros(len(kk), d, device="cuda")
+            for I in ri[cp[J]:cp[J + 1]]:
+                rr, keys, p, Dr = stats(int(I))
+                cols = torch.nonzero((keys >= J * B) & (keys < J * B + len(kk))).squeeze(1)
+                pj = p[:, cols]
+                dpj = dof[rr] @ vf[kk].T
+                dsj = pj * (dpj - Dr[:, None])
+                dv_w += pj.T @ dof[rr]
+                dk_w += (dsj.T @ qf[rr]) * scale
+            for name, got, want in (("dK", dk[h, kk], dk_w), ("dV", dv[h, kk], dv_w)):
+                rel = ((got.float() - want).norm() / want.norm()).item()
+                assert rel < BWD_REL_L2, f"{name} head {h} block {J}: {rel:.3e}"
