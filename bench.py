@@ -280,6 +280,26 @@ def run_ours(args, world, rank, local):
                  "dense_tflops": 4.0 * n * n * d * H / (dense_ms * 1e-3) / 1e12,
                  "speedup_sparse_vs_dense": dense_ms / kernel_ms, "steps": dsteps}
 
+    # backward (K3) over the same layout: algorithmic FLOPs = 2.5 x forward (5 GEMMs)
+    bwd = None
+    if args.bwd:
+        dout = torch.randn(Hl, n, d, device=dev, generator=g, dtype=torch.float32).to(torch.bfloat16)
+        P.masked_attention(q, k, v, lay, out=o, lse=lse, return_lse=True, stream=stream)
+
+        def bstep():
+            P.masked_attention_backward(q, k, v, o, lse, dout, lay, stream=stream)
+        for _ in range(max(1, args.warmup)):
+            bstep()
+        torch.cuda.synchronize()
+        bsteps = max(2, min(args.steps, 10))
+        bper = timed_loop(bstep, bsteps, stream)
+        bwd_ms = max_over_ranks(statistics.mean(bper), world)
+        bwd = {"ms_per_step": bwd_ms, "steps": bsteps,
+               "effective_tflops": 2.5 * flops_total / (bwd_ms * 1e-3) / 1e12,
+               "flops_convention": "2.5 x forward kept-block FLOPs (dQ, dK, dV, dP, S)",
+               "launches_per_step": 3}
+        del dout
+
     # end-to-end through the reference-facing C-ABI with host buffers
     e2e = None
     if not args.no_e2e:
@@ -331,6 +351,7 @@ def run_ours(args, world, rank, local):
                      "kernel": "radial_attn_fwd_kernel<128,128>",
                      "flops_per_launch": flops_local},
         "dense": dense,
+        "backward": bwd,
         "mask_build_ms": {"first": mask_ms_first, "warm_median": statistics.median(mts)},
         "e2e": e2e,
         "cpu_baseline": cpu,
@@ -379,6 +400,7 @@ def main():
     ap.add_argument("--no-dense", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--bwd", action="store_true", help="also time the backward (K3)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
