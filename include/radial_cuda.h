@@ -118,6 +118,11 @@ int radial_cuda_attn_fwd_host(const void* q, const void* k, const void* v, void*
                               uint32_t heads, uint64_t n, uint32_t head_dim, float scale,
                               const radial_layout* layout, void* stream);
 
+/* ---- host-buffer dense comparator (dense_attention's call shape, attention.hpp:141). */
+int radial_cuda_attn_fwd_dense_host(const void* q, const void* k, const void* v, void* o, float* lse,
+                                    uint32_t heads, uint64_t n, uint32_t head_dim, uint32_t block_size,
+                                    float scale, void* stream);
+
 /* ---- backward (no reference exists; SPEC.md:8 scopes training out): gradients
  *      of radial_cuda_attn_fwd over the same layout.  o / lse are the forward's
  *      outputs; dq/dk/dv are bf16 [heads][n][head_dim].  workspace: device

@@ -92,6 +92,45 @@ float resolve_scale(float scale, uint32_t D) {
     return scale > 0.f ? scale : static_cast<float>(1.0 / std::sqrt(static_cast<double>(D)));
 }
 
+// Host-buffer forward: H2D q/k/v, kernel (sparse when L != nullptr, else dense),
+// D2H o (+ lse), synchronise.  Device workspace cached per thread and device.
+int host_fwd(const void* q, const void* k, const void* v, void* o, float* lse, uint32_t heads,
+             uint64_t n, uint32_t head_dim, uint32_t BK, float scale, const radial_layout* L,
+             cudaStream_t st) {
+    thread_local void* ws = nullptr;
+    thread_local size_t ws_bytes = 0;
+    thread_local int ws_dev = -1;
+    int dev = 0;
+    RADIAL_CUDA_TRY(cudaGetDevice(&dev));
+    const size_t tbytes = static_cast<size_t>(heads) * n * head_dim * 2;
+    const size_t lbytes = static_cast<size_t>(heads) * n * 4;
+    const size_t need = 4 * tbytes + lbytes + 4096;
+    if (ws_bytes < need || ws_dev != dev) {
+        if (ws) cudaFree(ws);
+        ws = nullptr;
+        ws_bytes = 0;
+        RADIAL_CUDA_TRY(cudaMalloc(&ws, need));
+        ws_bytes = need;
+        ws_dev = dev;
+    }
+    auto* base = static_cast<uint8_t*>(ws);
+    void* dq = base;
+    void* dk = base + tbytes;
+    void* dv = base + 2 * tbytes;
+    void* dO = base + 3 * tbytes;
+    float* dl = reinterpret_cast<float*>(base + 4 * tbytes);
+    RADIAL_CUDA_TRY(cudaMemcpyAsync(dq, q, tbytes, cudaMemcpyHostToDevice, st));
+    RADIAL_CUDA_TRY(cudaMemcpyAsync(dk, k, tbytes, cudaMemcpyHostToDevice, st));
+    RADIAL_CUDA_TRY(cudaMemcpyAsync(dv, v, tbytes, cudaMemcpyHostToDevice, st));
+    int rc = launch_fwd(dq, dk, dv, dO, lse ? dl : nullptr, heads, n, head_dim, BK,
+                        resolve_scale(scale, head_dim), L, st);
+    if (rc) return rc;
+    RADIAL_CUDA_TRY(cudaMemcpyAsync(o, dO, tbytes, cudaMemcpyDeviceToHost, st));
+    if (lse) RADIAL_CUDA_TRY(cudaMemcpyAsync(lse, dl, lbytes, cudaMemcpyDeviceToHost, st));
+    RADIAL_CUDA_TRY(cudaStreamSynchronize(st));
+    return RADIAL_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -261,40 +300,19 @@ int radial_cuda_attn_fwd_host(const void* q, const void* k, const void* v, void*
     int rc = check_attn(q, k, v, o, heads, n, head_dim);
     if (rc) return rc;
     if ((rc = check_layout_for_attn(layout, n))) return rc;
-    // per-thread cached device workspace: q, k, v, o (bf16) + lse
-    thread_local void* ws = nullptr;
-    thread_local size_t ws_bytes = 0;
-    thread_local int ws_dev = -1;
-    int dev = 0;
-    RADIAL_CUDA_TRY(cudaGetDevice(&dev));
-    const size_t tbytes = static_cast<size_t>(heads) * n * head_dim * 2;
-    const size_t lbytes = static_cast<size_t>(heads) * n * 4;
-    const size_t need = 4 * tbytes + lbytes + 4096;
-    cudaStream_t st = static_cast<cudaStream_t>(stream);
-    if (ws_bytes < need || ws_dev != dev) {
-        if (ws) cudaFree(ws);
-        ws = nullptr;
-        ws_bytes = 0;
-        RADIAL_CUDA_TRY(cudaMalloc(&ws, need));
-        ws_bytes = need;
-        ws_dev = dev;
-    }
-    auto* base = static_cast<uint8_t*>(ws);
-    void* dq = base;
-    void* dk = base + tbytes;
-    void* dv = base + 2 * tbytes;
-    void* dO = base + 3 * tbytes;
-    float* dl = reinterpret_cast<float*>(base + 4 * tbytes);
-    RADIAL_CUDA_TRY(cudaMemcpyAsync(dq, q, tbytes, cudaMemcpyHostToDevice, st));
-    RADIAL_CUDA_TRY(cudaMemcpyAsync(dk, k, tbytes, cudaMemcpyHostToDevice, st));
-    RADIAL_CUDA_TRY(cudaMemcpyAsync(dv, v, tbytes, cudaMemcpyHostToDevice, st));
-    rc = launch_fwd(dq, dk, dv, dO, lse ? dl : nullptr, heads, n, head_dim, layout->B,
-                    resolve_scale(scale, head_dim), layout, st);
+    return host_fwd(q, k, v, o, lse, heads, n, head_dim, layout->B, scale, layout,
+                    static_cast<cudaStream_t>(stream));
+}
+
+int radial_cuda_attn_fwd_dense_host(const void* q, const void* k, const void* v, void* o, float* lse,
+                                    uint32_t heads, uint64_t n, uint32_t head_dim, uint32_t block_size,
+                                    float scale, void* stream) {
+    int rc = check_attn(q, k, v, o, heads, n, head_dim);
     if (rc) return rc;
-    RADIAL_CUDA_TRY(cudaMemcpyAsync(o, dO, tbytes, cudaMemcpyDeviceToHost, st));
-    if (lse) RADIAL_CUDA_TRY(cudaMemcpyAsync(lse, dl, lbytes, cudaMemcpyDeviceToHost, st));
-    RADIAL_CUDA_TRY(cudaStreamSynchronize(st));
-    return RADIAL_OK;
+    if (block_size != 64 && block_size != 128)
+        return fail(RADIAL_ERR_INVALID, "dense_attention: block_size must be 64 or 128");
+    return host_fwd(q, k, v, o, lse, heads, n, head_dim, block_size, scale, nullptr,
+                    static_cast<cudaStream_t>(stream));
 }
 
 size_t radial_cuda_attn_bwd_workspace_size(uint32_t heads, uint64_t n, uint32_t head_dim) {
