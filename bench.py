@@ -97,40 +97,32 @@ class ClockSampler:
                 "samples": len(self.samples)}
 
 
+_HP = None  # paper_2506_19852_b200.heads.HeadParallel of this process
+
+
 def dist_setup():
+    """One process per GPU; NCCL process group when launched by torchrun (N > 1)."""
+    global _HP
     import torch
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world > 1:
-        import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    elif torch.cuda.is_available():
+    from paper_2506_19852_b200.heads import HeadParallel
+    _HP = HeadParallel.from_env("nccl")
+    if _HP.world == 1 and torch.cuda.is_available():
         torch.cuda.set_device(0)
-    return world, rank, local
+    return _HP.world, _HP.rank, _HP.local_rank
 
 
 def barrier(world):
-    if world > 1:
-        import torch.distributed as dist
-        dist.barrier()
+    if _HP is not None:
+        _HP.barrier()
 
 
 def max_over_ranks(x: float, world: int) -> float:
-    if world == 1:
-        return x
-    import torch
-    import torch.distributed as dist
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    return float(t.item())
+    return _HP.max(x) if _HP is not None else x
 
 
 def head_slice(H, world, rank):
-    base, rem = divmod(H, world)
-    lo = rank * base + min(rank, rem)
-    return lo, lo + base + (1 if rank < rem else 0)
+    from paper_2506_19852_b200.heads import head_slice as hs
+    return hs(H, world, rank)
 
 
 def timed_loop(fn, steps, stream):
@@ -244,8 +236,14 @@ def run_ours(args, world, rank, local):
     o = torch.empty_like(q)
     lse = torch.empty(Hl, n, device=dev, dtype=torch.float32)
 
+    o_full = None
+    if args.gather and world > 1:
+        o_full = torch.empty(H, n, d, device=dev, dtype=torch.bfloat16)
+
     def step():
         P.masked_attention(q, k, v, lay, out=o, lse=lse, return_lse=True, stream=stream)
+        if o_full is not None:  # C1: reassemble O [H, n, d] on every rank over NVLink
+            _HP.gather_heads(o, H, out=o_full)
 
     for _ in range(args.warmup):
         step()
@@ -342,7 +340,7 @@ def run_ours(args, world, rank, local):
                                f"head_dim {d}, block {B}, sink on; heads split {Hl}/rank",
                    "frames": f, "tokens_per_frame": s, "heads": H, "head_dim": d, "block": B,
                    "kept_blocks": kept, "block_sparsity": 1 - kept / float(lay.grid_rows ** 2),
-                   "parallelism": f"head-parallel x{world}",
+                   "parallelism": f"head-parallel x{world}" + (" + all-gather(O)" if args.gather and world > 1 else ""),
                    "l2": "inputs (3 x bf16 [H][n][d]) far exceed the 126 MB L2; no flush"},
         "kernel_ms": kernel_ms,
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
@@ -401,6 +399,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--bwd", action="store_true", help="also time the backward (K3)")
+    ap.add_argument("--gather", action="store_true",
+                    help="include the NCCL all-gather of O (C1) in each step when N > 1")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -411,9 +411,7 @@ def main():
         return
     world, rank, local = dist_setup()
     run_ours(args, world, rank, local)
-    if world > 1:
-        import torch.distributed as dist
-        dist.destroy_process_group()
+    _HP.close()
 
 
 if __name__ == "__main__":
