@@ -95,7 +95,7 @@ struct FwdCfg {
 };
 
 template <int D, int BK>
-__global__ void __maxnreg__(112)
+__global__ void __maxnreg__(104)  // 18 warps x (104 + 2 reserved, rounded to 8) <= 64K registers
     radial_attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q,
                            const __grid_constant__ CUtensorMap tm_k,
                            const __grid_constant__ CUtensorMap tm_v, const FwdParams p) {
