@@ -95,7 +95,7 @@ struct FwdCfg {
 };
 
 template <int D, int BK>
-__global__ void __maxnreg__(104)  // 18 warps x (104 + 2 reserved, rounded to 8) <= 64K registers
+__global__ void __maxnreg__(96)  // 18 warps: 5 warps on some SM sub-partitions, 16K regs each -> <= 96
     radial_attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q,
                            const __grid_constant__ CUtensorMap tm_k,
                            const __grid_constant__ CUtensorMap tm_v, const FwdParams p) {
@@ -541,3 +541,16 @@ int launch_fwd(const void* q, const void* k, const void* v, void* o, float* lse,
 }
 
 }  // namespace radial_detail
+
+// Diagnostic hook: cudaFuncGetAttributes of the <128,128> forward kernel
+// (numRegs, maxThreadsPerBlock, sharedSizeBytes, maxDynamicSharedSizeBytes, localSizeBytes).
+extern "C" int radial_cuda_debug_fwd_attrs(int* out5) {
+    cudaFuncAttributes a{};
+    RADIAL_CUDA_TRY(cudaFuncGetAttributes(&a, radial_attn_fwd_kernel<128, 128>));
+    out5[0] = a.numRegs;
+    out5[1] = a.maxThreadsPerBlock;
+    out5[2] = static_cast<int>(a.sharedSizeBytes);
+    out5[3] = a.maxDynamicSharedSizeBytes;
+    out5[4] = static_cast<int>(a.localSizeBytes);
+    return RADIAL_OK;
+}
