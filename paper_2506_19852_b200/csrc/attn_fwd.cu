@@ -47,7 +47,7 @@ constexpr int kTraceCtas = 4, kTraceSteps = 64, kTraceEv = 16;
 
 namespace {
 
-constexpr int kThreads = 576;  // 18 warps: producer, MMA, 4 softmax warpgroups
+constexpr int kThreads = 384;
 constexpr uint32_t kTmem = 0;   // TMEM base address (checked against tcgen05.alloc)
 constexpr int kBQ = 128;        // query rows per tile
 constexpr int kStagesK = 2;   // the MMA loop is unrolled by the ring depth (2)
@@ -84,8 +84,7 @@ struct FwdCfg {
     static constexpr int kSmemV = kSmemK + kStagesK * kKVBytes;
     static constexpr int kSmemBar = kSmemV + kStagesV * kKVBytes;
     static constexpr int kNumBars = 1 + 2 * kStagesK + 2 * kStagesV + 2 + 4 + 2;
-    static constexpr int kSmemX = kSmemBar + 256;                 // row-max / row-sum exchange
-    static constexpr int kSmemBytes = kSmemX + 2 * 2 * 128 * 4;
+    static constexpr int kSmemBytes = kSmemBar + kNumBars * 8 + 16;
     static constexpr int kSmemAlloc = kSmemBytes + 1024;  // slack for 1024 B alignment
     // TMEM columns
     static constexpr uint32_t kColS0 = 0, kColS1 = BK, kColO0 = 2 * BK, kColO1 = 2 * BK + D;
@@ -95,7 +94,7 @@ struct FwdCfg {
 };
 
 template <int D, int BK>
-__global__ void __maxnreg__(96)  // 18 warps: 5 warps on some SM sub-partitions, 16K regs each -> <= 96
+__global__ void __launch_bounds__(kThreads, 1)
     radial_attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q,
                            const __grid_constant__ CUtensorMap tm_k,
                            const __grid_constant__ CUtensorMap tm_v, const FwdParams p) {
@@ -160,7 +159,7 @@ __global__ void __maxnreg__(96)  // 18 warps: 5 warps on some SM sub-partitions,
         tma_prefetch_desc(&tm_k);
         tma_prefetch_desc(&tm_v);
     }
-    if (warp == 0) tmem_alloc(tmem_slot, Cfg::kTmemCols);
+    if (warp == 2) tmem_alloc(tmem_slot, Cfg::kTmemCols);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -168,6 +167,10 @@ __global__ void __maxnreg__(96)  // 18 warps: 5 warps on some SM sub-partitions,
     // starts at lane 0 / column 0; the constant base keeps tcgen05 operands uniform.
     if (*tmem_slot != 0) __trap();
     constexpr uint32_t tmem = kTmem;
+    // producer / MMA / allocator warpgroup needs few registers; the two softmax
+    // warpgroups hold a 128-column S row each (384 x 168 = 128 x 104 + 256 x 200)
+    if (warp < 4) {
+        regs_dec<104>();
     if (warp == 0) {
         // ------------------------------------------------------------ producer
         if (lane == 0) {
@@ -231,8 +234,7 @@ __global__ void __maxnreg__(96)  // 18 warps: 5 warps on some SM sub-partitions,
                         tc_fence_after();
 #pragma unroll
                         for (int kk = h * (BK / 32); kk < (h + 1) * (BK / 32); ++kk)
-                            mma_ts(kTmem + o_col,
-                                   kTmem + p_col + (kk / (BK / 32)) * (BK / 2) + (kk % (BK / 32)) * 8,
+                            mma_ts(kTmem + o_col, kTmem + p_col + kk * 8,
                                    sdesc_sw128(vb + kk * 16 * 128, Cfg::kKVAtomBytes, 1024), Cfg::kIdescO,
                                    (acc | kk) ? 1u : 0u);
                     }
@@ -280,24 +282,15 @@ __global__ void __maxnreg__(96)  // 18 warps: 5 warps on some SM sub-partitions,
             mma_commit(&bar_ofull[0]);
             mma_commit(&bar_ofull[1]);
         }
+    }
     } else {
+        regs_inc<200>();
         // ------------------------------------------------------------ softmax
-        // 4 warpgroups: g = (warp-2)/4 -> Q tile t = g/2, S-column half h = g%2.  The two
-        // warpgroups of a tile share its 128 rows (same TMEM lanes, warp%4 = sub-partition),
-        // exchange the row max through shared memory, and each publishes its half of P.
-        const int g = (warp - 2) >> 2;
-        const int t = g >> 1, h = g & 1;
-        const int sub = warp & 3;
-        const int r = (sub << 5) + lane;               // row in tile = TMEM lane
-        const uint32_t lane_addr = static_cast<uint32_t>(sub * 32) << 16;
-        constexpr int HC = BK / 2;                      // S columns per warpgroup
-        constexpr int HD = D / 2;                       // O columns per warpgroup
-        const uint32_t s_col = t ? Cfg::kColS1 : Cfg::kColS0;
-        const uint32_t s_addr = tmem + lane_addr + s_col + h * HC;
-        const uint32_t p_addr = tmem + lane_addr + s_col + h * HC;  // P half h = first HC/2 cols of S half h
-        const uint32_t o_addr = tmem + lane_addr + (t ? Cfg::kColO1 : Cfg::kColO0) + h * HD;
-        float* xch = reinterpret_cast<float*>(smem + Cfg::kSmemX) + t * 256;  // [half][row]
-        const uint32_t bar_id = 1 + t;                   // named barrier of this tile's 256 threads
+        const int t = (warp - 4) >> 2;                 // Q tile
+        const int r = ((warp & 3) << 5) + lane;        // row in tile = TMEM lane
+        const uint32_t lane_addr = static_cast<uint32_t>((warp & 3) * 32) << 16;
+        const uint32_t s_addr = tmem + lane_addr + (t ? Cfg::kColS1 : Cfg::kColS0);
+        const uint32_t o_addr = tmem + lane_addr + (t ? Cfg::kColO1 : Cfg::kColO0);
         const int my_bit = t * Cfg::GT + r / BK;
         const uint64_t grow = row0 + t * kBQ + r;
         const float sl2 = p.scale_log2;
@@ -308,48 +301,47 @@ __global__ void __maxnreg__(96)  // 18 warps: 5 warps on some SM sub-partitions,
             const uint32_t mask = e >> 28;
             if (((mask >> (t * Cfg::GT)) & ((1u << Cfg::GT) - 1)) == 0) continue;
             const uint32_t J = e & 0x0FFFFFFFu;
-            if (sub == 0 && lane == 0 && h == 0) TRACE(4 * t + 0, j);
+            if ((warp & 3) == 0 && lane == 0) TRACE(4 * t + 0, j);
             mbar_wait(&bar_sfull[t], sphase);
-            if (sub == 0 && lane == 0 && h == 0) TRACE(4 * t + 1, j);
+            if ((warp & 3) == 0 && lane == 0) TRACE(4 * t + 1, j);
             sphase ^= 1;
             tc_fence_after();
-            const bool active = (mask >> my_bit) & 1;
-            const uint64_t kv0 = static_cast<uint64_t>(J) * BK + h * HC;
-            const int valid = (kv0 + HC <= p.n) ? HC : (kv0 < p.n ? static_cast<int>(p.n - kv0) : 0);
-            const bool full = active && valid == HC;  // common case: no per-column masking
-            // pass 1: row max of this half (S streamed from TMEM 32 columns at a time)
-            float mx = -INFINITY;
+            float s[BK];
 #pragma unroll
-            for (int c0 = 0; c0 < HC; c0 += 32) {
+            for (int c = 0; c < BK; c += 32) {
                 uint32_t u[32];
-                tmem_ld32(s_addr + c0, u);
-                tmem_wait_ld();
-                if (!full) {
+                tmem_ld32(s_addr + c, u);
 #pragma unroll
-                    for (int x = 0; x < 32; ++x)
-                        u[x] = (active && c0 + x < valid) ? u[x] : __float_as_uint(-INFINITY);
-                }
+                for (int x = 0; x < 32; ++x) s[c + x] = __uint_as_float(u[x]);
+            }
+            tmem_wait_ld();
+            const bool active = (mask >> my_bit) & 1;
+            const uint64_t kv0 = static_cast<uint64_t>(J) * BK;
+            const int valid = (kv0 + BK <= p.n) ? BK : static_cast<int>(p.n - kv0);
+            const bool full = active && valid == BK;  // common case: no per-column masking
+            float mx = -INFINITY;
+            if (full) {
+                // tree reduction: 8 independent chains instead of one 128-long chain
                 float mm[8];
 #pragma unroll
-                for (int x = 0; x < 8; ++x) mm[x] = __uint_as_float(u[x]);
+                for (int x = 0; x < 8; ++x) mm[x] = s[x];
 #pragma unroll
-                for (int c = 8; c < 32; c += 8)
+                for (int c = 8; c < BK; c += 8)
 #pragma unroll
-                    for (int x = 0; x < 8; ++x) mm[x] = fmaxf(mm[x], __uint_as_float(u[c + x]));
-                mx = fmaxf(mx, fmaxf(fmaxf(fmaxf(mm[0], mm[1]), fmaxf(mm[2], mm[3])),
-                                     fmaxf(fmaxf(mm[4], mm[5]), fmaxf(mm[6], mm[7]))));
+                    for (int x = 0; x < 8; ++x) mm[x] = fmaxf(mm[x], s[c + x]);
+                mx = fmaxf(fmaxf(fmaxf(mm[0], mm[1]), fmaxf(mm[2], mm[3])),
+                           fmaxf(fmaxf(mm[4], mm[5]), fmaxf(mm[6], mm[7])));
+            } else if (active) {
+#pragma unroll
+                for (int c = 0; c < BK; ++c) mx = fmaxf(mx, c < valid ? s[c] : -INFINITY);
             }
-            // row max across the two column halves
-            xch[h * 128 + r] = mx;
-            named_bar_sync(bar_id, 256);
-            mx = fmaxf(mx, xch[(h ^ 1) * 128 + r]);
             const float m_cand = mx * sl2;
             const bool need = active && (m == -INFINITY || m_cand > m + kRescaleThreshold);
             const bool rescale = need && m != -INFINITY;
             if (__any_sync(0xffffffffu, rescale)) {
                 const float alpha = rescale ? ex2(m - m_cand) : 1.f;
 #pragma unroll
-                for (int c = 0; c < HD; c += 32) {
+                for (int c = 0; c < D; c += 32) {
                     uint32_t u[32];
                     tmem_ld32(o_addr + c, u);
                     tmem_wait_ld();
@@ -360,33 +352,24 @@ __global__ void __maxnreg__(96)  // 18 warps: 5 warps on some SM sub-partitions,
                 if (rescale) l *= alpha;
             }
             if (need) m = m_cand;
-            // masked entries are -inf -> ex2 gives exactly 0; rows that never saw a kept
-            // block keep m = -inf, so subtract 0 instead (all their entries are -inf)
-            const float mb = (m == -INFINITY) ? 0.f : m;
+            // P is produced in two key halves, each published on its own barrier, so
+            // the MMA warp starts the first half of PV while the second half's
+            // exponentials are still being computed.
             float2 r2a = make_float2(0.f, 0.f), r2b = make_float2(0.f, 0.f);
-            const float2 sl = make_float2(sl2, sl2), nm = make_float2(-mb, -mb);
-            // pass 2: P = exp2(S*scale*log2e - m) per 32-column chunk, packed to bf16 and
-            // written over the chunk's own (already consumed) S columns
-            auto exps = [&](auto POLY) {
-                constexpr int NP = decltype(POLY)::value;
+            const float2 sl = make_float2(sl2, sl2), nm = make_float2(-m, -m);
 #pragma unroll
-                for (int c0 = 0; c0 < HC; c0 += 32) {
-                    uint32_t u[32];
-                    tmem_ld32(s_addr + c0, u);
-                    tmem_wait_ld();
-                    if (!full) {
+            for (int h = 0; h < 2; ++h) {
+                uint32_t pk[BK / 4];
+                if (full) {
+                    // FA4-style split: kPolyPairs of every 4 column pairs use a cubic exp2
+                    // on the FMA pipe, the rest MUFU.EX2; scale, polynomial and row sums
+                    // run as packed f32x2 ops.
 #pragma unroll
-                        for (int x = 0; x < 32; ++x)
-                            u[x] = (active && c0 + x < valid) ? u[x] : __float_as_uint(-INFINITY);
-                    }
-                    uint32_t pk[16];
-#pragma unroll
-                    for (int c = 0; c < 32; c += 2) {
-                        const float2 x =
-                            __ffma2_rn(make_float2(__uint_as_float(u[c]), __uint_as_float(u[c + 1])), sl, nm);
+                    for (int c = h * (BK / 2); c < (h + 1) * (BK / 2); c += 2) {
+                        const float2 x = __ffma2_rn(make_float2(s[c], s[c + 1]), sl, nm);
                         float2 pr;
-                        if (((c >> 1) & 3) < NP) {
-                            pr = ex2_poly2(x);  // FA4-style FMA-pipe exp2 for a share of columns
+                        if (((c >> 1) & 3) < kPolyPairs) {
+                            pr = ex2_poly2(x);
                         } else {
                             pr.x = ex2(x.x);
                             pr.y = ex2(x.y);
@@ -395,32 +378,38 @@ __global__ void __maxnreg__(96)  // 18 warps: 5 warps on some SM sub-partitions,
                             r2b = __fadd2_rn(r2b, pr);
                         else
                             r2a = __fadd2_rn(r2a, pr);
-                        pk[c / 2] = pack_bf16(pr.x, pr.y);
+                        pk[(c - h * (BK / 2)) / 2] = pack_bf16(pr.x, pr.y);
                     }
-                    tmem_st16(p_addr + c0 / 2, pk);
+                } else if (active) {
+#pragma unroll
+                    for (int c = h * (BK / 2); c < (h + 1) * (BK / 2); c += 2) {
+                        const float p0 = c < valid ? ex2(fmaf(s[c], sl2, -m)) : 0.f;
+                        const float p1 = c + 1 < valid ? ex2(fmaf(s[c + 1], sl2, -m)) : 0.f;
+                        r2a.x += p0;
+                        r2a.y += p1;
+                        pk[(c - h * (BK / 2)) / 2] = pack_bf16(p0, p1);
+                    }
+                } else {
+#pragma unroll
+                    for (int c = 0; c < BK / 4; ++c) pk[c] = 0u;
                 }
-            };
-            if (kPolyPairs > 0 && full)
-                exps(std::integral_constant<int, kPolyPairs>{});
-            else
-                exps(std::integral_constant<int, 0>{});
-            tmem_wait_st();
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&bar_pready[2 * t + h]);
-            if (sub == 0 && lane == 0) TRACE(4 * t + 2 + h, j);
+#pragma unroll
+                for (int c = 0; c < BK / 4; c += 16) tmem_st16(s_addr + h * (BK / 4) + c, pk + c);
+                tmem_wait_st();
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&bar_pready[2 * t + h]);
+                if ((warp & 3) == 0 && lane == 0) TRACE(4 * t + 2 + h, j);
+            }
             l += (r2a.x + r2a.y) + (r2b.x + r2b.y);
         }
         // ------------------------------------------------------------ epilogue
         mbar_wait(&bar_ofull[t], 0);
         tc_fence_after();
-        xch[h * 128 + r] = l;
-        named_bar_sync(bar_id, 256);
-        const float lt = l + xch[(h ^ 1) * 128 + r];
-        const float inv = lt > 0.f ? 1.f / lt : 0.f;
-        __nv_bfloat16* orow = p.o + (static_cast<uint64_t>(head) * p.n + grow) * D + h * HD;
+        const float inv = l > 0.f ? 1.f / l : 0.f;
+        __nv_bfloat16* orow = p.o + (static_cast<uint64_t>(head) * p.n + grow) * D;
 #pragma unroll
-        for (int c = 0; c < HD; c += 32) {
+        for (int c = 0; c < D; c += 32) {
             uint32_t u[32];
             tmem_ld32(o_addr + c, u);
             tmem_wait_ld();
@@ -434,13 +423,13 @@ __global__ void __maxnreg__(96)  // 18 warps: 5 warps on some SM sub-partitions,
                 for (int x = 0; x < 4; ++x) dst[x] = make_uint4(w[4 * x], w[4 * x + 1], w[4 * x + 2], w[4 * x + 3]);
             }
         }
-        if (h == 0 && p.lse && grow < p.n)
+        if (p.lse && grow < p.n)
             p.lse[static_cast<uint64_t>(head) * p.n + grow] =
-                lt > 0.f ? (m + __log2f(lt)) * 0.69314718055994531f : -INFINITY;
+                l > 0.f ? (m + __log2f(l)) * 0.69314718055994531f : -INFINITY;
     }
     tc_fence_before();
     __syncthreads();
-    if (warp == 0) {
+    if (warp == 2) {
         tc_fence_after();
         tmem_dealloc(*tmem_slot, Cfg::kTmemCols);
     }
