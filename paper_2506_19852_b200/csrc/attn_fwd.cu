@@ -319,22 +319,22 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint64_t kv0 = static_cast<uint64_t>(J) * BK;
             const int valid = (kv0 + BK <= p.n) ? BK : static_cast<int>(p.n - kv0);
             const bool full = active && valid == BK;  // common case: no per-column masking
-            float mx = -INFINITY;
-            if (full) {
-                // tree reduction: 8 independent chains instead of one 128-long chain
-                float mm[8];
+            if (!full) {
+                // rare (tail KV block, or a row whose query block skips J): mask in place so
+                // a single code path follows; masked entries become -inf -> exp2 = 0
 #pragma unroll
-                for (int x = 0; x < 8; ++x) mm[x] = s[x];
-#pragma unroll
-                for (int c = 8; c < BK; c += 8)
-#pragma unroll
-                    for (int x = 0; x < 8; ++x) mm[x] = fmaxf(mm[x], s[c + x]);
-                mx = fmaxf(fmaxf(fmaxf(mm[0], mm[1]), fmaxf(mm[2], mm[3])),
-                           fmaxf(fmaxf(mm[4], mm[5]), fmaxf(mm[6], mm[7])));
-            } else if (active) {
-#pragma unroll
-                for (int c = 0; c < BK; ++c) mx = fmaxf(mx, c < valid ? s[c] : -INFINITY);
+                for (int c = 0; c < BK; ++c) s[c] = (active && c < valid) ? s[c] : -INFINITY;
             }
+            // tree reduction: 8 independent chains instead of one 128-long chain
+            float mm[8];
+#pragma unroll
+            for (int x = 0; x < 8; ++x) mm[x] = s[x];
+#pragma unroll
+            for (int c = 8; c < BK; c += 8)
+#pragma unroll
+                for (int x = 0; x < 8; ++x) mm[x] = fmaxf(mm[x], s[c + x]);
+            const float mx = fmaxf(fmaxf(fmaxf(mm[0], mm[1]), fmaxf(mm[2], mm[3])),
+                                   fmaxf(fmaxf(mm[4], mm[5]), fmaxf(mm[6], mm[7])));
             const float m_cand = mx * sl2;
             const bool need = active && (m == -INFINITY || m_cand > m + kRescaleThreshold);
             const bool rescale = need && m != -INFINITY;
@@ -352,46 +352,31 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (rescale) l *= alpha;
             }
             if (need) m = m_cand;
+            // rows that never saw a kept block keep m = -inf; all their entries are -inf
+            const float mb = (m == -INFINITY) ? 0.f : m;
             // P is produced in two key halves, each published on its own barrier, so
             // the MMA warp starts the first half of PV while the second half's
             // exponentials are still being computed.
             float2 r2a = make_float2(0.f, 0.f), r2b = make_float2(0.f, 0.f);
-            const float2 sl = make_float2(sl2, sl2), nm = make_float2(-m, -m);
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
+            const float2 sl = make_float2(sl2, sl2), nm = make_float2(-mb, -mb);
+            auto half = [&](int h, auto POLY) {
+                constexpr int NP = decltype(POLY)::value;
                 uint32_t pk[BK / 4];
-                if (full) {
-                    // FA4-style split: kPolyPairs of every 4 column pairs use a cubic exp2
-                    // on the FMA pipe, the rest MUFU.EX2; scale, polynomial and row sums
-                    // run as packed f32x2 ops.
 #pragma unroll
-                    for (int c = h * (BK / 2); c < (h + 1) * (BK / 2); c += 2) {
-                        const float2 x = __ffma2_rn(make_float2(s[c], s[c + 1]), sl, nm);
-                        float2 pr;
-                        if (((c >> 1) & 3) < kPolyPairs) {
-                            pr = ex2_poly2(x);
-                        } else {
-                            pr.x = ex2(x.x);
-                            pr.y = ex2(x.y);
-                        }
-                        if ((c >> 1) & 1)
-                            r2b = __fadd2_rn(r2b, pr);
-                        else
-                            r2a = __fadd2_rn(r2a, pr);
-                        pk[(c - h * (BK / 2)) / 2] = pack_bf16(pr.x, pr.y);
+                for (int c = h * (BK / 2); c < (h + 1) * (BK / 2); c += 2) {
+                    const float2 x = __ffma2_rn(make_float2(s[c], s[c + 1]), sl, nm);
+                    float2 pr;
+                    if (((c >> 1) & 3) < NP) {
+                        pr = ex2_poly2(x);  // FA4-style FMA-pipe exp2 for a share of columns
+                    } else {
+                        pr.x = ex2(x.x);
+                        pr.y = ex2(x.y);
                     }
-                } else if (active) {
-#pragma unroll
-                    for (int c = h * (BK / 2); c < (h + 1) * (BK / 2); c += 2) {
-                        const float p0 = c < valid ? ex2(fmaf(s[c], sl2, -m)) : 0.f;
-                        const float p1 = c + 1 < valid ? ex2(fmaf(s[c + 1], sl2, -m)) : 0.f;
-                        r2a.x += p0;
-                        r2a.y += p1;
-                        pk[(c - h * (BK / 2)) / 2] = pack_bf16(p0, p1);
-                    }
-                } else {
-#pragma unroll
-                    for (int c = 0; c < BK / 4; ++c) pk[c] = 0u;
+                    if ((c >> 1) & 1)
+                        r2b = __fadd2_rn(r2b, pr);
+                    else
+                        r2a = __fadd2_rn(r2a, pr);
+                    pk[(c - h * (BK / 2)) / 2] = pack_bf16(pr.x, pr.y);
                 }
 #pragma unroll
                 for (int c = 0; c < BK / 4; c += 16) tmem_st16(s_addr + h * (BK / 4) + c, pk + c);
@@ -400,6 +385,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&bar_pready[2 * t + h]);
                 if ((warp & 3) == 0 && lane == 0) TRACE(4 * t + 2 + h, j);
+            };
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                if (kPolyPairs > 0 && full)
+                    half(h, std::integral_constant<int, kPolyPairs>{});
+                else
+                    half(h, std::integral_constant<int, 0>{});
             }
             l += (r2a.x + r2a.y) + (r2b.x + r2b.y);
         }
