@@ -204,9 +204,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (lane == 0) {
             mbar_wait(bar_q, 0);
             tc_fence_after();
-            const uint32_t q_base = smem_u32(smem + Cfg::kSmemQ);
-            const uint32_t k_base = smem_u32(smem + Cfg::kSmemK);
-            const uint32_t v_base = smem_u32(smem + Cfg::kSmemV);
+            // base descriptors; an MMA's descriptor = base + (byte offset >> 4) (the 14-bit
+            // start-address field cannot carry: every offset stays inside 256 KB)
+            const uint64_t dq = sdesc_sw128(smem_u32(smem + Cfg::kSmemQ), 16, 1024);
+            const uint64_t dk = sdesc_sw128(smem_u32(smem + Cfg::kSmemK), 16, 1024);
+            const uint64_t dv = sdesc_sw128(smem_u32(smem + Cfg::kSmemV), Cfg::kKVAtomBytes, 1024);
             bool pend0 = false, pend1 = false;
             uint32_t acc0 = 0, acc1 = 0;
             uint32_t pphase0 = 0, pphase1 = 0;
@@ -226,7 +228,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     constexpr int T = decltype(TC)::value;
                     constexpr uint32_t p_col = T ? Cfg::kColS1 : Cfg::kColS0;
                     constexpr uint32_t o_col = T ? Cfg::kColO1 : Cfg::kColO0;
-                    const uint32_t vb = v_base + VSP * Cfg::kKVBytes;
+
 #pragma unroll
                     for (int h = 0; h < 2; ++h) {
                         mbar_wait(&bar_pready[2 * T + h], pphase);
@@ -235,7 +237,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                         for (int kk = h * (BK / 32); kk < (h + 1) * (BK / 32); ++kk)
                             mma_ts(kTmem + o_col, kTmem + p_col + kk * 8,
-                                   sdesc_sw128(vb + kk * 16 * 128, Cfg::kKVAtomBytes, 1024), Cfg::kIdescO,
+                                   dv + ((VSP * Cfg::kKVBytes + kk * 16 * 128) >> 4), Cfg::kIdescO,
                                    (acc | kk) ? 1u : 0u);
                     }
                     pphase ^= 1;
@@ -244,14 +246,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                 auto qk = [&](auto TC) {
                     constexpr int T = decltype(TC)::value;
                     constexpr uint32_t s_col = T ? Cfg::kColS1 : Cfg::kColS0;
-                    const uint32_t qb = q_base + T * Cfg::kQBytes;
-                    const uint32_t kb = k_base + KS * Cfg::kKVBytes;
+
 #pragma unroll
                     for (int kk = 0; kk < D / 16; ++kk) {
                         const uint32_t off_q = (kk >> 2) * Cfg::kQAtomBytes + (kk & 3) * 32;
                         const uint32_t off_k = (kk >> 2) * Cfg::kKVAtomBytes + (kk & 3) * 32;
-                        mma_ss(kTmem + s_col, sdesc_sw128(qb + off_q, 16, 1024),
-                               sdesc_sw128(kb + off_k, 16, 1024), Cfg::kIdescS, kk ? 1u : 0u);
+                        mma_ss(kTmem + s_col, dq + ((T * Cfg::kQBytes + off_q) >> 4),
+                               dk + ((KS * Cfg::kKVBytes + off_k) >> 4), Cfg::kIdescS, kk ? 1u : 0u);
                     }
                     mma_commit(&bar_sfull[T]);
                     TRACE(12 + T, j);
