@@ -280,82 +280,158 @@ __global__ void __launch_bounds__(1024) scan_rows(const uint32_t* __restrict__ c
     }
 }
 
-// Builds ptr/idx lists for `rows` rows over `cols` columns with predicate F.
+// Stable argsort of rows by list length, longest first (LPT work order), one CTA.
+// keys = ptr[i+1] - ptr[i]; n <= kSortMax (bitonic sort in shared memory).
+constexpr int kSortMax = 4096;  // 32 KB of static shared memory
+__global__ void __launch_bounds__(1024) lpt_sort_kernel(const uint64_t* __restrict__ ptr, uint32_t n,
+                                                        uint32_t* __restrict__ order) {
+    __shared__ unsigned long long key[kSortMax];  // (max_len - len) << 32 | index: ascending sort
+    uint32_t m = 1;
+    while (m < n) m <<= 1;
+    for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) {
+        if (i < n) {
+            const uint64_t len = ptr[i + 1] - ptr[i];
+            key[i] = (static_cast<unsigned long long>(0xffffffffu - static_cast<uint32_t>(len)) << 32) | i;
+        } else {
+            key[i] = ~0ull;
+        }
+    }
+    __syncthreads();
+    for (uint32_t k = 2; k <= m; k <<= 1) {
+        for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+            for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) {
+                const uint32_t ixj = i ^ j;
+                if (ixj > i) {
+                    const unsigned long long a = key[i], b = key[ixj];
+                    const bool up = (i & k) == 0;
+                    if ((a > b) == up) {
+                        key[i] = b;
+                        key[ixj] = a;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    }
+    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) order[i] = static_cast<uint32_t>(key[i] & 0xffffffffu);
+}
+
+// One list family (rows x cols under predicate F): counts -> exclusive scan into ptr.
 template <class F>
-int build_lists(F pred, uint32_t rows, uint32_t cols, int with_mask, cudaStream_t st,
-                uint64_t** ptr_out, uint32_t** idx_out, ScanStats* host_stats) {
-    uint32_t* counts = nullptr;
-    ScanStats* dstats = nullptr;
-    RADIAL_CUDA_TRY(cudaMallocAsync(&counts, sizeof(uint32_t) * std::max<uint32_t>(rows, 1), st));
-    RADIAL_CUDA_TRY(cudaMallocAsync(&dstats, sizeof(ScanStats), st));
-    RADIAL_CUDA_TRY(cudaMalloc(ptr_out, sizeof(uint64_t) * (static_cast<size_t>(rows) + 1)));
+int count_and_scan(F pred, uint32_t rows, uint32_t cols, uint32_t* counts, uint64_t* ptr, ScanStats* dstats,
+                   cudaStream_t st) {
     if (rows) list_count<F><<<rows, kThreads, 0, st>>>(pred, cols, counts);
-    scan_rows<<<1, 1024, 0, st>>>(counts, rows, *ptr_out, dstats);
+    scan_rows<<<1, 1024, 0, st>>>(counts, rows, ptr, dstats);
     RADIAL_CUDA_TRY(cudaGetLastError());
-    RADIAL_CUDA_TRY(cudaMemcpyAsync(host_stats, dstats, sizeof(ScanStats), cudaMemcpyDeviceToHost, st));
-    RADIAL_CUDA_TRY(cudaStreamSynchronize(st));
-    RADIAL_CUDA_TRY(cudaMalloc(idx_out, sizeof(uint32_t) * std::max<uint64_t>(host_stats->nnz, 1)));
-    if (rows) list_fill<F><<<rows, kThreads, 0, st>>>(pred, cols, *ptr_out, *idx_out, with_mask);
-    RADIAL_CUDA_TRY(cudaGetLastError());
-    RADIAL_CUDA_TRY(cudaFreeAsync(counts, st));
-    RADIAL_CUDA_TRY(cudaFreeAsync(dstats, st));
     return RADIAL_OK;
 }
 
-// Longest-processing-time-first order of chunks (by work-list length).
-int lpt_order(const uint64_t* dptr, uint32_t C, cudaStream_t st, uint32_t** order_out) {
-    std::vector<uint64_t> h(C + 1);
-    RADIAL_CUDA_TRY(cudaMemcpyAsync(h.data(), dptr, sizeof(uint64_t) * (C + 1), cudaMemcpyDeviceToHost, st));
+template <class F>
+int fill(F pred, uint32_t rows, uint32_t cols, const uint64_t* ptr, uint32_t* idx, int with_mask,
+         cudaStream_t st) {
+    if (rows) list_fill<F><<<rows, kThreads, 0, st>>>(pred, cols, ptr, idx, with_mask);
+    RADIAL_CUDA_TRY(cudaGetLastError());
+    return RADIAL_OK;
+}
+
+// Longest-processing-time-first order of `n` lists (device sort; host fallback when large).
+int lpt_order(const uint64_t* dptr, uint32_t n, cudaStream_t st, uint32_t** order_out) {
+    RADIAL_CUDA_TRY(cudaMalloc(order_out, sizeof(uint32_t) * std::max<uint32_t>(n, 1)));
+    if (n == 0) return RADIAL_OK;
+    if (n <= static_cast<uint32_t>(kSortMax)) {
+        lpt_sort_kernel<<<1, 1024, 0, st>>>(dptr, n, *order_out);
+        RADIAL_CUDA_TRY(cudaGetLastError());
+        return RADIAL_OK;
+    }
+    std::vector<uint64_t> h(n + 1);
+    RADIAL_CUDA_TRY(cudaMemcpyAsync(h.data(), dptr, sizeof(uint64_t) * (n + 1), cudaMemcpyDeviceToHost, st));
     RADIAL_CUDA_TRY(cudaStreamSynchronize(st));
-    std::vector<uint32_t> ord(C);
+    std::vector<uint32_t> ord(n);
     std::iota(ord.begin(), ord.end(), 0u);
-    std::stable_sort(ord.begin(), ord.end(), [&](uint32_t a, uint32_t b) {
-        return (h[a + 1] - h[a]) > (h[b + 1] - h[b]);
-    });
-    RADIAL_CUDA_TRY(cudaMalloc(order_out, sizeof(uint32_t) * std::max<uint32_t>(C, 1)));
-    RADIAL_CUDA_TRY(cudaMemcpyAsync(*order_out, ord.data(), sizeof(uint32_t) * C, cudaMemcpyHostToDevice, st));
+    std::stable_sort(ord.begin(), ord.end(),
+                     [&](uint32_t a, uint32_t b) { return (h[a + 1] - h[a]) > (h[b + 1] - h[b]); });
+    RADIAL_CUDA_TRY(cudaMemcpyAsync(*order_out, ord.data(), sizeof(uint32_t) * n, cudaMemcpyHostToDevice, st));
     RADIAL_CUDA_TRY(cudaStreamSynchronize(st));
     return RADIAL_OK;
 }
+
+struct Scratch {
+    uint32_t* counts = nullptr;
+    ScanStats* stats = nullptr;  // [4] CSR, CSC, query-chunk unions, KV-chunk unions
+    ScanStats* host = nullptr;   // pinned
+    ~Scratch() {
+        if (counts) cudaFree(counts);
+        if (stats) cudaFree(stats);
+        if (host) cudaFreeHost(host);
+    }
+};
 
 }  // namespace
 
 namespace radial_detail {
 
+// K1: CSR of the pattern by the closed-form block predicate.  One host sync (nnz).
 int build_layout_device(radial_layout* L, cudaStream_t st) {
     MaskParams p{L->f, L->s, L->B, static_cast<uint64_t>(L->f) * L->s, L->kind, L->sink, L->tw, L->sw};
-    ScanStats hs{};
-    int rc = build_lists(BlockKeep{p}, L->R, L->R, 0, st, &L->row_ptr, &L->col_idx, &hs);
+    Scratch sc;
+    RADIAL_CUDA_TRY(cudaMalloc(&sc.counts, sizeof(uint32_t) * std::max<uint32_t>(L->R, 1)));
+    RADIAL_CUDA_TRY(cudaMalloc(&sc.stats, sizeof(ScanStats)));
+    RADIAL_CUDA_TRY(cudaMallocHost(&sc.host, sizeof(ScanStats)));
+    RADIAL_CUDA_TRY(cudaMalloc(&L->row_ptr, sizeof(uint64_t) * (static_cast<size_t>(L->R) + 1)));
+    int rc = count_and_scan(BlockKeep{p}, L->R, L->R, sc.counts, L->row_ptr, sc.stats, st);
     if (rc) return rc;
-    L->nnz = hs.nnz;
-    L->first_empty_row = hs.first_empty;
-    L->max_row_len = hs.max_len;
-    L->min_row_len = hs.min_len;
-    return RADIAL_OK;
+    RADIAL_CUDA_TRY(cudaMemcpyAsync(sc.host, sc.stats, sizeof(ScanStats), cudaMemcpyDeviceToHost, st));
+    RADIAL_CUDA_TRY(cudaStreamSynchronize(st));
+    L->nnz = sc.host->nnz;
+    L->first_empty_row = sc.host->first_empty;
+    L->max_row_len = sc.host->max_len;
+    L->min_row_len = sc.host->min_len;
+    RADIAL_CUDA_TRY(cudaMalloc(&L->col_idx, sizeof(uint32_t) * std::max<uint64_t>(L->nnz, 1)));
+    return fill(BlockKeep{p}, L->R, L->R, L->row_ptr, L->col_idx, 0, st);
 }
 
+// CSC, chunk unions and LPT orders for a CSR already on the device.  One host sync
+// (union sizes) plus a final one so the handle is complete when this returns.
 int build_worklists(radial_layout* L, cudaStream_t st) {
-    ScanStats hs{};
-    int rc = build_lists(CsrTranspose{L->row_ptr, L->col_idx}, L->R, L->R, 0, st, &L->col_ptr,
-                         &L->row_idx, &hs);
-    if (rc) return rc;
-    if (hs.nnz != L->nnz) return fail(RADIAL_ERR_INVALID, "layout transpose size mismatch");
-    if (L->B != 64 && L->B != 128) return RADIAL_OK;  // attention kernels not instantiated
-    rc = lpt_order(L->row_ptr, L->R, st, &L->rorder);
-    if (rc) return rc;
-    rc = lpt_order(L->col_ptr, L->R, st, &L->corder);
-    if (rc) return rc;
-    L->G = 256 / L->B;
-    L->C = (L->R + L->G - 1) / L->G;
-    rc = build_lists(ChunkUnion{L->row_ptr, L->col_idx, L->R, L->G}, L->C, L->R, 1, st, &L->uptr,
-                     &L->uidx, &hs);
-    if (rc) return rc;
-    rc = lpt_order(L->uptr, L->C, st, &L->uorder);
-    if (rc) return rc;
-    rc = build_lists(ChunkUnion{L->col_ptr, L->row_idx, L->R, L->G}, L->C, L->R, 1, st, &L->tptr,
-                     &L->tidx, &hs);
-    if (rc) return rc;
-    return lpt_order(L->tptr, L->C, st, &L->torder);
+    Scratch sc;
+    const uint32_t R = L->R;
+    const bool attn = (L->B == 64 || L->B == 128);
+    L->G = attn ? 256 / L->B : 1;
+    L->C = attn ? (R + L->G - 1) / L->G : 0;
+    const uint32_t C = L->C;
+    RADIAL_CUDA_TRY(cudaMalloc(&sc.counts, sizeof(uint32_t) * (std::max<uint32_t>(R, 1) + 2 * std::max<uint32_t>(C, 1))));
+    RADIAL_CUDA_TRY(cudaMalloc(&sc.stats, 4 * sizeof(ScanStats)));
+    RADIAL_CUDA_TRY(cudaMallocHost(&sc.host, 4 * sizeof(ScanStats)));
+    RADIAL_CUDA_TRY(cudaMalloc(&L->col_ptr, sizeof(uint64_t) * (static_cast<size_t>(R) + 1)));
+    RADIAL_CUDA_TRY(cudaMalloc(&L->row_idx, sizeof(uint32_t) * std::max<uint64_t>(L->nnz, 1)));
+    int rc;
+    // CSC: its nnz equals the CSR's, so no sync is needed before the fill
+    const CsrTranspose tr{L->row_ptr, L->col_idx};
+    if ((rc = count_and_scan(tr, R, R, sc.counts, L->col_ptr, sc.stats + 1, st))) return rc;
+    if ((rc = fill(tr, R, R, L->col_ptr, L->row_idx, 0, st))) return rc;
+    if (!attn) {
+        RADIAL_CUDA_TRY(cudaStreamSynchronize(st));
+        return RADIAL_OK;  // attention kernels not instantiated for this block size
+    }
+    RADIAL_CUDA_TRY(cudaMalloc(&L->uptr, sizeof(uint64_t) * (static_cast<size_t>(C) + 1)));
+    RADIAL_CUDA_TRY(cudaMalloc(&L->tptr, sizeof(uint64_t) * (static_cast<size_t>(C) + 1)));
+    const ChunkUnion uq{L->row_ptr, L->col_idx, R, L->G};
+    const ChunkUnion ukv{L->col_ptr, L->row_idx, R, L->G};
+    if ((rc = count_and_scan(uq, C, R, sc.counts + R, L->uptr, sc.stats + 2, st))) return rc;
+    if ((rc = count_and_scan(ukv, C, R, sc.counts + R + C, L->tptr, sc.stats + 3, st))) return rc;
+    if ((rc = lpt_order(L->row_ptr, R, st, &L->rorder))) return rc;
+    if ((rc = lpt_order(L->col_ptr, R, st, &L->corder))) return rc;
+    if ((rc = lpt_order(L->uptr, C, st, &L->uorder))) return rc;
+    if ((rc = lpt_order(L->tptr, C, st, &L->torder))) return rc;
+    RADIAL_CUDA_TRY(cudaMemcpyAsync(sc.host, sc.stats, 4 * sizeof(ScanStats), cudaMemcpyDeviceToHost, st));
+    RADIAL_CUDA_TRY(cudaStreamSynchronize(st));
+    if (sc.host[1].nnz != L->nnz) return fail(RADIAL_ERR_INVALID, "layout transpose size mismatch");
+    RADIAL_CUDA_TRY(cudaMalloc(&L->uidx, sizeof(uint32_t) * std::max<uint64_t>(sc.host[2].nnz, 1)));
+    RADIAL_CUDA_TRY(cudaMalloc(&L->tidx, sizeof(uint32_t) * std::max<uint64_t>(sc.host[3].nnz, 1)));
+    if ((rc = fill(uq, C, R, L->uptr, L->uidx, 1, st))) return rc;
+    if ((rc = fill(ukv, C, R, L->tptr, L->tidx, 1, st))) return rc;
+    RADIAL_CUDA_TRY(cudaStreamSynchronize(st));
+    return RADIAL_OK;
 }
 
 }  // namespace radial_detail
