@@ -336,7 +336,7 @@ int fill(F pred, uint32_t rows, uint32_t cols, const uint64_t* ptr, uint32_t* id
 
 // Longest-processing-time-first order of `n` lists (device sort; host fallback when large).
 int lpt_order(const uint64_t* dptr, uint32_t n, cudaStream_t st, uint32_t** order_out) {
-    RADIAL_CUDA_TRY(cudaMalloc(order_out, sizeof(uint32_t) * std::max<uint32_t>(n, 1)));
+    RADIAL_CUDA_TRY(cudaMallocAsync(order_out, sizeof(uint32_t) * std::max<uint32_t>(n, 1), st));
     if (n == 0) return RADIAL_OK;
     if (n <= static_cast<uint32_t>(kSortMax)) {
         lpt_sort_kernel<<<1, 1024, 0, st>>>(dptr, n, *order_out);
@@ -355,14 +355,16 @@ int lpt_order(const uint64_t* dptr, uint32_t n, cudaStream_t st, uint32_t** orde
     return RADIAL_OK;
 }
 
+// Stream-ordered scratch (pool allocations; no device-wide synchronisation).
 struct Scratch {
+    cudaStream_t st;
     uint32_t* counts = nullptr;
     ScanStats* stats = nullptr;  // [4] CSR, CSC, query-chunk unions, KV-chunk unions
-    ScanStats* host = nullptr;   // pinned
+    ScanStats host[4];
+    explicit Scratch(cudaStream_t s) : st(s) {}
     ~Scratch() {
-        if (counts) cudaFree(counts);
-        if (stats) cudaFree(stats);
-        if (host) cudaFreeHost(host);
+        if (counts) cudaFreeAsync(counts, st);
+        if (stats) cudaFreeAsync(stats, st);
     }
 };
 
@@ -373,37 +375,35 @@ namespace radial_detail {
 // K1: CSR of the pattern by the closed-form block predicate.  One host sync (nnz).
 int build_layout_device(radial_layout* L, cudaStream_t st) {
     MaskParams p{L->f, L->s, L->B, static_cast<uint64_t>(L->f) * L->s, L->kind, L->sink, L->tw, L->sw};
-    Scratch sc;
-    RADIAL_CUDA_TRY(cudaMalloc(&sc.counts, sizeof(uint32_t) * std::max<uint32_t>(L->R, 1)));
-    RADIAL_CUDA_TRY(cudaMalloc(&sc.stats, sizeof(ScanStats)));
-    RADIAL_CUDA_TRY(cudaMallocHost(&sc.host, sizeof(ScanStats)));
-    RADIAL_CUDA_TRY(cudaMalloc(&L->row_ptr, sizeof(uint64_t) * (static_cast<size_t>(L->R) + 1)));
+    Scratch sc(st);
+    RADIAL_CUDA_TRY(cudaMallocAsync(&sc.counts, sizeof(uint32_t) * std::max<uint32_t>(L->R, 1), st));
+    RADIAL_CUDA_TRY(cudaMallocAsync(&sc.stats, sizeof(ScanStats), st));
+    RADIAL_CUDA_TRY(cudaMallocAsync(&L->row_ptr, sizeof(uint64_t) * (static_cast<size_t>(L->R) + 1), st));
     int rc = count_and_scan(BlockKeep{p}, L->R, L->R, sc.counts, L->row_ptr, sc.stats, st);
     if (rc) return rc;
     RADIAL_CUDA_TRY(cudaMemcpyAsync(sc.host, sc.stats, sizeof(ScanStats), cudaMemcpyDeviceToHost, st));
     RADIAL_CUDA_TRY(cudaStreamSynchronize(st));
-    L->nnz = sc.host->nnz;
-    L->first_empty_row = sc.host->first_empty;
-    L->max_row_len = sc.host->max_len;
-    L->min_row_len = sc.host->min_len;
-    RADIAL_CUDA_TRY(cudaMalloc(&L->col_idx, sizeof(uint32_t) * std::max<uint64_t>(L->nnz, 1)));
+    L->nnz = sc.host[0].nnz;
+    L->first_empty_row = sc.host[0].first_empty;
+    L->max_row_len = sc.host[0].max_len;
+    L->min_row_len = sc.host[0].min_len;
+    RADIAL_CUDA_TRY(cudaMallocAsync(&L->col_idx, sizeof(uint32_t) * std::max<uint64_t>(L->nnz, 1), st));
     return fill(BlockKeep{p}, L->R, L->R, L->row_ptr, L->col_idx, 0, st);
 }
 
 // CSC, chunk unions and LPT orders for a CSR already on the device.  One host sync
 // (union sizes) plus a final one so the handle is complete when this returns.
 int build_worklists(radial_layout* L, cudaStream_t st) {
-    Scratch sc;
+    Scratch sc(st);
     const uint32_t R = L->R;
     const bool attn = (L->B == 64 || L->B == 128);
     L->G = attn ? 256 / L->B : 1;
     L->C = attn ? (R + L->G - 1) / L->G : 0;
     const uint32_t C = L->C;
-    RADIAL_CUDA_TRY(cudaMalloc(&sc.counts, sizeof(uint32_t) * (std::max<uint32_t>(R, 1) + 2 * std::max<uint32_t>(C, 1))));
-    RADIAL_CUDA_TRY(cudaMalloc(&sc.stats, 4 * sizeof(ScanStats)));
-    RADIAL_CUDA_TRY(cudaMallocHost(&sc.host, 4 * sizeof(ScanStats)));
-    RADIAL_CUDA_TRY(cudaMalloc(&L->col_ptr, sizeof(uint64_t) * (static_cast<size_t>(R) + 1)));
-    RADIAL_CUDA_TRY(cudaMalloc(&L->row_idx, sizeof(uint32_t) * std::max<uint64_t>(L->nnz, 1)));
+    RADIAL_CUDA_TRY(cudaMallocAsync(&sc.counts, sizeof(uint32_t) * (std::max<uint32_t>(R, 1) + 2 * std::max<uint32_t>(C, 1)), st));
+    RADIAL_CUDA_TRY(cudaMallocAsync(&sc.stats, 4 * sizeof(ScanStats), st));
+    RADIAL_CUDA_TRY(cudaMallocAsync(&L->col_ptr, sizeof(uint64_t) * (static_cast<size_t>(R) + 1), st));
+    RADIAL_CUDA_TRY(cudaMallocAsync(&L->row_idx, sizeof(uint32_t) * std::max<uint64_t>(L->nnz, 1), st));
     int rc;
     // CSC: its nnz equals the CSR's, so no sync is needed before the fill
     const CsrTranspose tr{L->row_ptr, L->col_idx};
@@ -413,8 +413,8 @@ int build_worklists(radial_layout* L, cudaStream_t st) {
         RADIAL_CUDA_TRY(cudaStreamSynchronize(st));
         return RADIAL_OK;  // attention kernels not instantiated for this block size
     }
-    RADIAL_CUDA_TRY(cudaMalloc(&L->uptr, sizeof(uint64_t) * (static_cast<size_t>(C) + 1)));
-    RADIAL_CUDA_TRY(cudaMalloc(&L->tptr, sizeof(uint64_t) * (static_cast<size_t>(C) + 1)));
+    RADIAL_CUDA_TRY(cudaMallocAsync(&L->uptr, sizeof(uint64_t) * (static_cast<size_t>(C) + 1), st));
+    RADIAL_CUDA_TRY(cudaMallocAsync(&L->tptr, sizeof(uint64_t) * (static_cast<size_t>(C) + 1), st));
     const ChunkUnion uq{L->row_ptr, L->col_idx, R, L->G};
     const ChunkUnion ukv{L->col_ptr, L->row_idx, R, L->G};
     if ((rc = count_and_scan(uq, C, R, sc.counts + R, L->uptr, sc.stats + 2, st))) return rc;
@@ -426,8 +426,8 @@ int build_worklists(radial_layout* L, cudaStream_t st) {
     RADIAL_CUDA_TRY(cudaMemcpyAsync(sc.host, sc.stats, 4 * sizeof(ScanStats), cudaMemcpyDeviceToHost, st));
     RADIAL_CUDA_TRY(cudaStreamSynchronize(st));
     if (sc.host[1].nnz != L->nnz) return fail(RADIAL_ERR_INVALID, "layout transpose size mismatch");
-    RADIAL_CUDA_TRY(cudaMalloc(&L->uidx, sizeof(uint32_t) * std::max<uint64_t>(sc.host[2].nnz, 1)));
-    RADIAL_CUDA_TRY(cudaMalloc(&L->tidx, sizeof(uint32_t) * std::max<uint64_t>(sc.host[3].nnz, 1)));
+    RADIAL_CUDA_TRY(cudaMallocAsync(&L->uidx, sizeof(uint32_t) * std::max<uint64_t>(sc.host[2].nnz, 1), st));
+    RADIAL_CUDA_TRY(cudaMallocAsync(&L->tidx, sizeof(uint32_t) * std::max<uint64_t>(sc.host[3].nnz, 1), st));
     if ((rc = fill(uq, C, R, L->uptr, L->uidx, 1, st))) return rc;
     if ((rc = fill(ukv, C, R, L->tptr, L->tidx, 1, st))) return rc;
     RADIAL_CUDA_TRY(cudaStreamSynchronize(st));

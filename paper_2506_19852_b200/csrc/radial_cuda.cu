@@ -38,6 +38,9 @@ namespace {
 
 void free_layout(radial_layout* L) {
     if (!L) return;
+    // stream-ordered (pool) allocations are not implicitly synchronised by cudaFree:
+    // drain any in-flight kernel that may still read the layout
+    cudaDeviceSynchronize();
     void* ptrs[] = {L->row_ptr, L->col_idx, L->col_ptr, L->row_idx, L->uptr,   L->uidx,
                     L->uorder,  L->tptr,    L->tidx,    L->torder,  L->rorder, L->corder};
     for (void* p : ptrs)
