@@ -104,6 +104,14 @@ int radial_cuda_attn_fwd(const void* q, const void* k, const void* v, void* o, f
                          uint32_t heads, uint64_t n, uint32_t head_dim, float scale,
                          const radial_layout* layout, void* stream);
 
+/* ---- token-exact forward: replaces radial::masked_attention(const AttentionInstance&,
+ *      const PatternSpec&) (attention.hpp:184-225).  Iterates the blocks of a layout built
+ *      by radial_cuda_mask_build (a superset, block.hpp:59) and keeps exactly the token
+ *      pairs of the pattern's rule (mask.hpp:105-154, 238-272).  Frame-structured kinds only. */
+int radial_cuda_attn_fwd_token(const void* q, const void* k, const void* v, void* o, float* lse,
+                               uint32_t heads, uint64_t n, uint32_t head_dim, float scale,
+                               const radial_layout* layout, void* stream);
+
 /* ---- dense comparator: replaces radial::dense_attention (attention.hpp:141-163),
  *      same kernel over every KV block; block_size picks the KV tile (64/128). */
 int radial_cuda_attn_fwd_dense(const void* q, const void* k, const void* v, void* o, float* lse,

@@ -58,6 +58,9 @@ def _load_c():
         fn.restype = _i32
         fn.argtypes = [_u64, _u32, fp, fp, fp, _u32, C.c_void_p, C.c_void_p, _u64p, _u64, _f64,
                        _f64p, C.c_void_p, C.POINTER(_u64)]
+    lib.ro_token_attention_rows_f32.restype = _i32
+    lib.ro_token_attention_rows_f32.argtypes = [_u64, _u32, _f32p, _f32p, _f32p, _u32, _u32, _i32, _i32,
+                                                _u32, _u32, _u64p, _u64, _f64, _f64p, C.c_void_p]
     lib.ro_attention_bwd_f32.restype = _i32
     lib.ro_attention_bwd_f32.argtypes = [_u64, _u32, _f32p, _f32p, _f32p, _f32p, _u32, C.c_void_p,
                                          C.c_void_p, _f64, _f64p, _f64p, _f64p]
@@ -82,6 +85,9 @@ def _load_ref():
     lib.ref_dense_attention.argtypes = [_u32, _u32, _u32, _f64p, _f64p, _f64p, _f64p]
     lib.ref_attention_flops.restype = _i32
     lib.ref_attention_flops.argtypes = [_u32, _u32, _u32, _i32, _u32, _u32] + [C.POINTER(_f64)] * 4
+    lib.ref_masked_attention_pattern.restype = _i32
+    lib.ref_masked_attention_pattern.argtypes = [_u32, _u32, _u32, _f64p, _f64p, _f64p, _i32, _i32, _u32,
+                                                 _u32, _f64p]
     lib.ref_instance_create.restype = C.c_void_p
     lib.ref_instance_create.argtypes = [_u32, _u32, _u32, _u64]
     lib.ref_instance_free.restype = None
@@ -213,6 +219,36 @@ def attention_rows(q, k, v, B, row_ptr, col_idx, rows, scale=0.0, want_lse=False
     if st == 2:
         raise RuntimeError(f"masked_attention: query row {bad.value} keeps no keys")
     return (out, lse) if want_lse else out
+
+
+def token_attention_rows(q, k, v, f, s, rows, kind="radial", sink=True, tw=0, sw=0, scale=0.0,
+                         want_lse=False):
+    """fp64 restatement of masked_attention(inst, PatternSpec) (attention.hpp:184-225), the
+    token-exact path, for the given query rows (fp32 inputs)."""
+    n, d = q.shape
+    rows = np.ascontiguousarray(rows, np.uint64)
+    out = np.zeros((len(rows), d), np.float64)
+    lse = np.zeros(len(rows), np.float64) if want_lse else None
+    f32 = lambda x: np.ascontiguousarray(x, np.float32)
+    st = c().ro_token_attention_rows_f32(n, d, f32(q), f32(k), f32(v), f, s, KIND[kind], int(sink), tw,
+                                         sw, rows, len(rows), scale, out,
+                                         None if lse is None else lse.ctypes.data)
+    if st != 0:
+        raise RuntimeError("token_attention_rows failed")
+    return (out, lse) if want_lse else out
+
+
+def ref_masked_attention_pattern(f, s, q, k, v, kind="radial", sink=True, tw=0, sw=0):
+    """The reference's own token-exact masked_attention(inst, PatternSpec)."""
+    n, d = q.shape
+    out = np.zeros((n, d), np.float64)
+    st = ref().ref_masked_attention_pattern(f, s, d, np.ascontiguousarray(q, np.float64),
+                                            np.ascontiguousarray(k, np.float64),
+                                            np.ascontiguousarray(v, np.float64), KIND[kind], int(sink),
+                                            tw, sw, out)
+    if st != 0:
+        raise RuntimeError(ref().ref_last_error().decode())
+    return out
 
 
 def attention_bwd(q, k, v, do, B, row_ptr, col_idx, scale=0.0):

@@ -529,3 +529,69 @@ int ro_attention_bwd_f32(uint64_t n, uint32_t d, const float* q, const float* k,
 }
 
 int ro_version(void) { return 1; }
+
+/* ------------------------------------------------------------------------ */
+/* attention.hpp:184-225  masked_attention(inst, PatternSpec): token-exact   */
+/* softmax over the keys of for_each_kept_interval (mask.hpp:238-272), for   */
+/* frame-structured kinds, restated for chosen query rows. fp32 inputs.      */
+/* ------------------------------------------------------------------------ */
+typedef struct {
+    uint64_t n;
+    uint32_t d, f, s;
+    const float *q, *k, *v;
+    ro_pattern pat;
+    const uint64_t* rows;
+    double* out;
+    double* lse;
+    double scale;
+    int status;
+} ro_tok_ctx;
+
+static void ro_tok_row(void* vctx, uint64_t r) {
+    ro_tok_ctx* c = (ro_tok_ctx*)vctx;
+    const uint64_t u = c->rows[r];
+    const uint32_t d = c->d, s = c->s;
+    const uint32_t i = (uint32_t)(u / s), kpos = (uint32_t)(u % s);
+    double* o = c->out + r * d;
+    for (uint32_t e = 0; e < d; ++e) o[e] = 0.0;
+    double m = -INFINITY;
+    /* pass 1: max over kept logits */
+    for (uint32_t j = 0; j < c->f; ++j) {
+        uint32_t lo, hi;
+        if (ro_kept_span(c->pat.kind, c->pat.sink, c->pat.tw, c->pat.sw, s, i, kpos, kpos, j, &lo, &hi) != 1) continue;
+        for (uint64_t v = (uint64_t)j * s + lo; v <= (uint64_t)j * s + hi; ++v) {
+            double dot = 0.0;
+            for (uint32_t x = 0; x < d; ++x) dot += (double)c->q[u * d + x] * (double)c->k[v * d + x];
+            if (dot * c->scale > m) m = dot * c->scale;
+        }
+    }
+    if (m == -INFINITY) {
+        c->status = 2;
+        return;
+    }
+    double denom = 0.0;
+    for (uint32_t j = 0; j < c->f; ++j) {
+        uint32_t lo, hi;
+        if (ro_kept_span(c->pat.kind, c->pat.sink, c->pat.tw, c->pat.sw, s, i, kpos, kpos, j, &lo, &hi) != 1) continue;
+        for (uint64_t v = (uint64_t)j * s + lo; v <= (uint64_t)j * s + hi; ++v) {
+            double dot = 0.0;
+            for (uint32_t x = 0; x < d; ++x) dot += (double)c->q[u * d + x] * (double)c->k[v * d + x];
+            double w = exp(dot * c->scale - m);
+            denom += w;
+            for (uint32_t x = 0; x < d; ++x) o[x] += w * (double)c->v[v * d + x];
+        }
+    }
+    for (uint32_t x = 0; x < d; ++x) o[x] /= denom;
+    if (c->lse) c->lse[r] = m + log(denom);
+}
+
+int ro_token_attention_rows_f32(uint64_t n, uint32_t d, const float* q, const float* k, const float* v,
+                                uint32_t f, uint32_t s, int kind, int sink, uint32_t tw, uint32_t sw,
+                                const uint64_t* rows, uint64_t n_rows, double scale, double* out,
+                                double* lse) {
+    ro_tok_ctx c = {n, d, f, s, q, k, v, {kind, sink, 1, 1, tw, sw}, rows, out, lse,
+                    scale > 0 ? scale : 1.0 / sqrt((double)d), 0};
+    if (kind == RO_KIND_POWER) return -1;
+    ro_parallel_for(n_rows, ro_tok_row, &c);
+    return c.status;
+}

@@ -207,3 +207,30 @@ int ref_masked_attention_inst(void* inst_p, uint32_t B, uint32_t R, const uint64
 }
 
 }  // extern "C"
+
+// radial::masked_attention(const AttentionInstance&, const PatternSpec&)
+// (attention.hpp:184) -- the token-exact reference.
+extern "C" int ref_masked_attention_pattern(uint32_t f, uint32_t s, uint32_t d, const double* q,
+                                            const double* k, const double* v, int kind, int sink,
+                                            uint32_t tw, uint32_t sw, double* out) {
+    try {
+        radial::GridShape shape(f, s);
+        const std::size_t n = shape.total_tokens();
+        radial::AttentionInstance inst;
+        inst.shape = shape;
+        inst.head_dim = d;
+        inst.query = radial::Matrix(n, d);
+        inst.key = radial::Matrix(n, d);
+        inst.value = radial::Matrix(n, d);
+        std::memcpy(inst.query.data.data(), q, n * d * sizeof(double));
+        std::memcpy(inst.key.data.data(), k, n * d * sizeof(double));
+        std::memcpy(inst.value.data.data(), v, n * d * sizeof(double));
+        auto o = radial::masked_attention(inst, make_pattern(kind, sink, tw, sw));
+        std::memcpy(out, o.data.data(), n * d * sizeof(double));
+        return 0;
+    } catch (const std::invalid_argument& e) {
+        return fail(e, 1);
+    } catch (const std::exception& e) {
+        return fail(e, 2);
+    }
+}

@@ -40,7 +40,7 @@ import numpy as np
 __all__ = [
     "GridShape", "PatternSpec", "PatternKind", "BlockLayout", "DeviceLayout", "FlopsReport",
     "LengthError", "ParseError", "blockify", "device_layout", "masked_attention",
-    "dense_attention", "masked_attention_backward", "masked_attention_host", "attention_flops",
+    "dense_attention", "masked_attention_backward", "masked_attention_pattern", "masked_attention_host", "attention_flops",
     "sparsity", "serialize", "deserialize", "library_path",
 ]
 
@@ -88,6 +88,7 @@ _sig("radial_cuda_layout_copy_csc", _i32, _vp, _vp, _vp)
 _sig("radial_cuda_layout_device_csr", _i32, _vp, C.POINTER(_vp), C.POINTER(_vp))
 _sig("radial_cuda_layout_free", None, _vp)
 _sig("radial_cuda_attn_fwd", _i32, _vp, _vp, _vp, _vp, _vp, _u32, _u64, _u32, _f32, _vp, _vp)
+_sig("radial_cuda_attn_fwd_token", _i32, _vp, _vp, _vp, _vp, _vp, _u32, _u64, _u32, _f32, _vp, _vp)
 _sig("radial_cuda_attn_fwd_dense", _i32, _vp, _vp, _vp, _vp, _vp, _u32, _u64, _u32, _u32, _f32, _vp)
 _sig("radial_cuda_attn_fwd_host", _i32, _vp, _vp, _vp, _vp, _vp, _u32, _u64, _u32, _f32, _vp, _vp)
 _sig("radial_cuda_attn_bwd_workspace_size", C.c_size_t, _u32, _u64, _u32)
@@ -485,6 +486,26 @@ def masked_attention(q, k, v, layout, scale: Optional[float] = None, *, out=None
     _check(_lib.radial_cuda_attn_fwd(q.data_ptr(), k.data_ptr(), v.data_ptr(), o.data_ptr(),
                                      lse.data_ptr() if lse is not None else None, H, n, d,
                                      float(scale or 0.0), L.handle, _stream_ptr(stream)))
+    return (o, lse) if return_lse else o
+
+
+def masked_attention_pattern(q, k, v, shape: GridShape, pattern: PatternSpec, scale: Optional[float] = None,
+                             *, block_size: int = 128, out=None, lse=None, return_lse: bool = False,
+                             stream=None):
+    """radial::masked_attention(inst, PatternSpec) (attention.hpp:184-225): the token-exact
+    mask (no block over-approximation).  The kernel walks the blocks of the pattern's
+    block layout and keeps exactly the token pairs of the keep rule (mask.hpp:105-154)."""
+    import torch
+    H, n, d = _check_qkv(q, k, v)
+    if shape.total_tokens() != n:
+        raise ValueError("masked_attention: layout shape mismatch")
+    L = device_layout(shape, pattern, block_size, stream=stream)
+    o = out if out is not None else torch.empty_like(q)
+    if return_lse and lse is None:
+        lse = torch.empty((H, n), dtype=torch.float32, device=q.device)
+    _check(_lib.radial_cuda_attn_fwd_token(q.data_ptr(), k.data_ptr(), v.data_ptr(), o.data_ptr(),
+                                           lse.data_ptr() if lse is not None else None, H, n, d,
+                                           float(scale or 0.0), L.handle, _stream_ptr(stream)))
     return (o, lse) if return_lse else o
 
 

@@ -24,6 +24,7 @@
 #include <cmath>
 #include <type_traits>
 
+#include "mask_rule.cuh"
 #include "radial_internal.h"
 #include "sm100.cuh"
 
@@ -68,6 +69,7 @@ struct FwdParams {
     uint32_t heads, R, C;
     float scale_log2;
     int dense;
+    radial_rule::MaskParams rule;  // token-exact mode: the pattern's keep rule
 };
 
 template <int D, int BK>
@@ -93,7 +95,7 @@ struct FwdCfg {
     static constexpr uint32_t kIdescO = idesc_bf16(128, D, 0, 1);
 };
 
-template <int D, int BK>
+template <int D, int BK, bool TOKEN>
 __global__ void __launch_bounds__(kThreads, 1)
     radial_attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q,
                            const __grid_constant__ CUtensorMap tm_k,
@@ -294,6 +296,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t o_addr = tmem + lane_addr + (t ? Cfg::kColO1 : Cfg::kColO0);
         const int my_bit = t * Cfg::GT + r / BK;
         const uint64_t grow = row0 + t * kBQ + r;
+        // token coordinates (frame, position) of this row, for the token-exact mode
+        const uint32_t tok_i = TOKEN ? static_cast<uint32_t>(grow / p.rule.s) : 0u;
+        const uint32_t tok_k = TOKEN ? static_cast<uint32_t>(grow % p.rule.s) : 0u;
         const float sl2 = p.scale_log2;
         float m = -INFINITY, l = 0.f;
         uint32_t sphase = 0;
@@ -319,12 +324,48 @@ __global__ void __launch_bounds__(kThreads, 1)
             const bool active = (mask >> my_bit) & 1;
             const uint64_t kv0 = static_cast<uint64_t>(J) * BK;
             const int valid = (kv0 + BK <= p.n) ? BK : static_cast<int>(p.n - kv0);
-            const bool full = active && valid == BK;  // common case: no per-column masking
-            if (!full) {
-                // rare (tail KV block, or a row whose query block skips J): mask in place so
-                // a single code path follows; masked entries become -inf -> exp2 = 0
+            bool full = active && valid == BK;  // common case: no per-column masking
+            uint32_t kmask[BK / 32];
+            if constexpr (TOKEN) {
+                // token-exact mode (masked_attention(inst, PatternSpec), attention.hpp:184-225):
+                // keep exactly the key intervals kept_span(i, k, k, j) of this row's token
+                // (i, k) in each key frame j the block overlaps (mask.hpp:238-272)
 #pragma unroll
-                for (int c = 0; c < BK; ++c) s[c] = (active && c < valid) ? s[c] : -INFINITY;
+                for (int w = 0; w < BK / 32; ++w) kmask[w] = 0u;
+                if (active && grow < p.n) {
+                    const uint32_t v0 = J * BK, v1 = v0 + static_cast<uint32_t>(valid) - 1;
+                    for (uint32_t jf = v0 / p.rule.s; jf * p.rule.s <= v1; ++jf) {
+                        uint32_t lo, hi;
+                        if (!radial_rule::kept_span(p.rule, tok_i, tok_k, tok_k, jf, lo, hi)) continue;
+                        const uint32_t a = max(jf * p.rule.s + lo, v0) - v0;
+                        const uint32_t b = min(jf * p.rule.s + hi, v1);
+                        if (b < v0 || a > b - v0) continue;
+                        const uint32_t bb = b - v0;
+#pragma unroll
+                        for (int w = 0; w < BK / 32; ++w) {
+                            const int lw = max(static_cast<int>(a), 32 * w), hw = min(static_cast<int>(bb), 32 * w + 31);
+                            if (lw <= hw) {
+                                const int len = hw - lw + 1;
+                                kmask[w] |= (len == 32 ? 0xffffffffu : ((1u << len) - 1u)) << (lw - 32 * w);
+                            }
+                        }
+                    }
+                }
+                bool all = true;
+#pragma unroll
+                for (int w = 0; w < BK / 32; ++w) all = all && kmask[w] == 0xffffffffu;
+                full = active && all;
+            }
+            if (!full) {
+                // rare (tail KV block, a row whose query block skips J, or a token-masked
+                // entry): mask in place so a single code path follows; masked entries
+                // become -inf -> exp2 = 0
+#pragma unroll
+                for (int c = 0; c < BK; ++c) {
+                    bool keep = c < valid;
+                    if constexpr (TOKEN) keep = (kmask[c >> 5] >> (c & 31)) & 1u;
+                    s[c] = (active && keep) ? s[c] : -INFINITY;
+                }
             }
             // tree reduction: 8 independent chains instead of one 128-long chain
             float mm[8];
@@ -471,7 +512,7 @@ int make_tmap_bf16_3d(CUtensorMap* m, const void* base, uint64_t n, uint32_t D, 
 template <int D, int BK>
 int launch_fwd_t(const void* q, const void* k, const void* v, void* o, float* lse,
                  uint32_t heads, uint64_t n, float scale, const radial_layout* L, uint32_t R,
-                 cudaStream_t st) {
+                 bool token, cudaStream_t st) {
     using Cfg = FwdCfg<D, BK>;
     CUtensorMap tq, tk, tv;
     int rc;
@@ -492,7 +533,10 @@ int launch_fwd_t(const void* q, const void* k, const void* v, void* o, float* ls
         p.uidx = L->uidx;
         p.order = L->uorder;
     }
-    auto kern = radial_attn_fwd_kernel<D, BK>;
+    if (token) {
+        p.rule = radial_rule::MaskParams{L->f, L->s, L->B, n, L->kind, L->sink, L->tw, L->sw};
+    }
+    auto kern = token ? radial_attn_fwd_kernel<D, BK, true> : radial_attn_fwd_kernel<D, BK, false>;
     RADIAL_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmemAlloc));
     const uint64_t items = static_cast<uint64_t>(p.C) * heads;
     if (items == 0) return RADIAL_OK;
@@ -511,14 +555,14 @@ extern "C" int radial_cuda_debug_trace(void* buf) {
 
 int launch_fwd(const void* q, const void* k, const void* v, void* o, float* lse, uint32_t heads,
                uint64_t n, uint32_t D, uint32_t BK, float scale, const radial_layout* L,
-               cudaStream_t st) {
+               cudaStream_t st, bool token) {
     const uint64_t R64 = (n + BK - 1) / BK;
     if (R64 >= (1ull << 28)) return fail(RADIAL_ERR_INVALID, "block grid too large for the kernel");
     const uint32_t R = static_cast<uint32_t>(R64);
-    if (D == 128 && BK == 128) return launch_fwd_t<128, 128>(q, k, v, o, lse, heads, n, scale, L, R, st);
-    if (D == 128 && BK == 64) return launch_fwd_t<128, 64>(q, k, v, o, lse, heads, n, scale, L, R, st);
-    if (D == 64 && BK == 128) return launch_fwd_t<64, 128>(q, k, v, o, lse, heads, n, scale, L, R, st);
-    if (D == 64 && BK == 64) return launch_fwd_t<64, 64>(q, k, v, o, lse, heads, n, scale, L, R, st);
+    if (D == 128 && BK == 128) return launch_fwd_t<128, 128>(q, k, v, o, lse, heads, n, scale, L, R, token, st);
+    if (D == 128 && BK == 64) return launch_fwd_t<128, 64>(q, k, v, o, lse, heads, n, scale, L, R, token, st);
+    if (D == 64 && BK == 128) return launch_fwd_t<64, 128>(q, k, v, o, lse, heads, n, scale, L, R, token, st);
+    if (D == 64 && BK == 64) return launch_fwd_t<64, 64>(q, k, v, o, lse, heads, n, scale, L, R, token, st);
     return fail(RADIAL_ERR_INVALID, "masked_attention: head_dim must be 64 or 128 and block_size 64 or 128");
 }
 
@@ -528,7 +572,7 @@ int launch_fwd(const void* q, const void* k, const void* v, void* o, float* lse,
 // (numRegs, maxThreadsPerBlock, sharedSizeBytes, maxDynamicSharedSizeBytes, localSizeBytes).
 extern "C" int radial_cuda_debug_fwd_attrs(int* out5) {
     cudaFuncAttributes a{};
-    RADIAL_CUDA_TRY(cudaFuncGetAttributes(&a, radial_attn_fwd_kernel<128, 128>));
+    RADIAL_CUDA_TRY(cudaFuncGetAttributes(&a, radial_attn_fwd_kernel<128, 128, false>));
     out5[0] = a.numRegs;
     out5[1] = a.maxThreadsPerBlock;
     out5[2] = static_cast<int>(a.sharedSizeBytes);

@@ -20,80 +20,15 @@
 #include <numeric>
 #include <vector>
 
+#include "mask_rule.cuh"
 #include "radial_internal.h"
 
 namespace {
 
+using radial_rule::MaskParams;
+using radial_rule::kept_span;
+
 constexpr int kThreads = 256;
-
-struct MaskParams {
-    uint32_t f, s, B;
-    uint64_t n;
-    int kind, sink;
-    uint32_t tw, sw;
-};
-
-// mask.hpp:105-154 kept_span for every frame-structured kind.
-__device__ __forceinline__ bool kept_span(const MaskParams& p, uint32_t i, uint32_t k_lo,
-                                          uint32_t k_hi, uint32_t j, uint32_t& lo, uint32_t& hi) {
-    const uint32_t s = p.s;
-    const uint64_t d = i < j ? j - i : i - j;
-    auto band = [&](uint32_t sigma) {
-        lo = k_lo > sigma ? k_lo - sigma : 0;
-        uint64_t h = static_cast<uint64_t>(k_hi) + sigma;
-        hi = h >= s ? s - 1 : static_cast<uint32_t>(h);
-        return true;
-    };
-    if (p.sink && j == 0) {
-        lo = 0;
-        hi = s - 1;
-        return true;
-    }
-    switch (p.kind) {
-        case RADIAL_KIND_DENSE:
-            lo = 0;
-            hi = s - 1;
-            return true;
-        case RADIAL_KIND_RADIAL: {
-            const uint32_t e = d <= 1 ? 0u : 63u - __clzll(d);
-            const uint64_t pw = 1ull << e;
-            if (pw <= s) return band(static_cast<uint32_t>(s / pw) - 1);
-            const uint64_t period = (pw + s - 1) / s;
-            if (d % period == 0) {
-                lo = k_lo;
-                hi = k_hi;
-                return true;
-            }
-            return false;
-        }
-        case RADIAL_KIND_SPATIAL:
-            if (d <= p.tw) {
-                lo = 0;
-                hi = s - 1;
-                return true;
-            }
-            return false;
-        case RADIAL_KIND_TEMPORAL:
-            return band(min(p.sw, s - 1));
-        case RADIAL_KIND_STA:
-            if (d <= p.tw) return band(min(p.sw, s - 1));
-            return false;
-        case RADIAL_KIND_HARMONIC: {
-            const uint64_t dist = d < 1 ? 1 : d;
-            const uint64_t width = s / dist;
-            if (width >= 1) return band(static_cast<uint32_t>(width) - 1);
-            const uint64_t period = (dist + s - 1) / s;
-            if (d % period == 0) {
-                lo = k_lo;
-                hi = k_hi;
-                return true;
-            }
-            return false;
-        }
-        default:
-            return false;
-    }
-}
 
 // Block (I, J) kept?  Frame-structured kinds: exact per-pair restatement of
 // the painting in block.hpp:81-97.  Power: block-level rule block.hpp:71-80.

@@ -1,0 +1,91 @@
+// mask_rule.cuh -- the reference keep rule on the device, shared by K1 (block
+// layouts) and the token-exact forward.  Restates detail::kept_span
+// (/root/reference/proj/include/radial/mask.hpp:105-154) for every
+// frame-structured kind: for query frame i, query positions [k_lo, k_hi] and key
+// frame j, the single kept key-position interval of frame j (or none).
+#pragma once
+
+#include <cstdint>
+
+#include "../../include/radial_cuda.h"
+
+namespace radial_rule {
+
+struct MaskParams {
+    uint32_t f, s, B;
+    uint64_t n;
+    int kind, sink;
+    uint32_t tw, sw;
+};
+
+__host__ __device__ __forceinline__ uint32_t floor_log2_u64(uint64_t x) {
+#ifdef __CUDA_ARCH__
+    return 63u - __clzll(static_cast<long long>(x));
+#else
+    return 63u - static_cast<uint32_t>(__builtin_clzll(x));
+#endif
+}
+
+// mask.hpp:105-154 kept_span for every frame-structured kind.
+__host__ __device__ __forceinline__ bool kept_span(const MaskParams& p, uint32_t i, uint32_t k_lo,
+                                          uint32_t k_hi, uint32_t j, uint32_t& lo, uint32_t& hi) {
+    const uint32_t s = p.s;
+    const uint64_t d = i < j ? j - i : i - j;
+    auto band = [&](uint32_t sigma) {
+        lo = k_lo > sigma ? k_lo - sigma : 0;
+        uint64_t h = static_cast<uint64_t>(k_hi) + sigma;
+        hi = h >= s ? s - 1 : static_cast<uint32_t>(h);
+        return true;
+    };
+    if (p.sink && j == 0) {
+        lo = 0;
+        hi = s - 1;
+        return true;
+    }
+    switch (p.kind) {
+        case RADIAL_KIND_DENSE:
+            lo = 0;
+            hi = s - 1;
+            return true;
+        case RADIAL_KIND_RADIAL: {
+            const uint32_t e = d <= 1 ? 0u : floor_log2_u64(d);
+            const uint64_t pw = 1ull << e;
+            if (pw <= s) return band(static_cast<uint32_t>(s / pw) - 1);
+            const uint64_t period = (pw + s - 1) / s;
+            if (d % period == 0) {
+                lo = k_lo;
+                hi = k_hi;
+                return true;
+            }
+            return false;
+        }
+        case RADIAL_KIND_SPATIAL:
+            if (d <= p.tw) {
+                lo = 0;
+                hi = s - 1;
+                return true;
+            }
+            return false;
+        case RADIAL_KIND_TEMPORAL:
+            return band((p.sw < s - 1 ? p.sw : s - 1));
+        case RADIAL_KIND_STA:
+            if (d <= p.tw) return band((p.sw < s - 1 ? p.sw : s - 1));
+            return false;
+        case RADIAL_KIND_HARMONIC: {
+            const uint64_t dist = d < 1 ? 1 : d;
+            const uint64_t width = s / dist;
+            if (width >= 1) return band(static_cast<uint32_t>(width) - 1);
+            const uint64_t period = (dist + s - 1) / s;
+            if (d % period == 0) {
+                lo = k_lo;
+                hi = k_hi;
+                return true;
+            }
+            return false;
+        }
+        default:
+            return false;
+    }
+}
+
+}  // namespace radial_rule

@@ -24,7 +24,7 @@ int cuda_fail(cudaError_t e, const char* where) {
 
 int launch_fwd(const void* q, const void* k, const void* v, void* o, float* lse, uint32_t heads,
                uint64_t n, uint32_t D, uint32_t BK, float scale, const radial_layout* L,
-               cudaStream_t st);
+               cudaStream_t st, bool token = false);
 int launch_bwd(const void* q, const void* k, const void* v, const void* o, const float* lse,
                const void* dout, void* dq, void* dk, void* dv, uint32_t heads, uint64_t n,
                uint32_t D, float scale, const radial_layout* L, void* workspace, cudaStream_t st);
@@ -159,6 +159,7 @@ int radial_cuda_mask_build(uint32_t frames, uint32_t tokens_per_frame, uint32_t 
     L->sink = sink ? 1 : 0;
     L->tw = temporal_window;
     L->sw = spatial_window;
+    L->from_pattern = 1;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     if ((rc = build_layout_device(L, st)) || (rc = build_worklists(L, st))) {
         free_layout(L);
@@ -284,6 +285,20 @@ int radial_cuda_attn_fwd(const void* q, const void* k, const void* v, void* o, f
     if ((rc = check_layout_for_attn(layout, n))) return rc;
     return launch_fwd(q, k, v, o, lse, heads, n, head_dim, layout->B, resolve_scale(scale, head_dim), layout,
                       static_cast<cudaStream_t>(stream));
+}
+
+int radial_cuda_attn_fwd_token(const void* q, const void* k, const void* v, void* o, float* lse,
+                               uint32_t heads, uint64_t n, uint32_t head_dim, float scale,
+                               const radial_layout* layout, void* stream) {
+    int rc = check_attn(q, k, v, o, heads, n, head_dim);
+    if (rc) return rc;
+    if ((rc = check_layout_for_attn(layout, n))) return rc;
+    if (layout->kind == RADIAL_KIND_POWER)
+        return fail(RADIAL_ERR_INVALID, "masked_attention: the power pattern has no per-frame span on the device path");
+    if (!layout->from_pattern)
+        return fail(RADIAL_ERR_INVALID, "masked_attention: token-exact mode needs a layout built by radial_cuda_mask_build");
+    return launch_fwd(q, k, v, o, lse, heads, n, head_dim, layout->B, resolve_scale(scale, head_dim), layout,
+                      static_cast<cudaStream_t>(stream), true);
 }
 
 int radial_cuda_attn_fwd_dense(const void* q, const void* k, const void* v, void* o, float* lse,

@@ -15,6 +15,7 @@ struct radial_layout {
     uint32_t f = 1, s = 1, B = 1, R = 0;
     uint8_t kind = 0, sink = 1;
     uint32_t tw = 0, sw = 0;
+    int from_pattern = 0;   // built by radial_cuda_mask_build (pattern parameters known)
     uint64_t nnz = 0;
     int64_t first_empty_row = -1;
     uint32_t max_row_len = 0, min_row_len = 0;

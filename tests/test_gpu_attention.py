@@ -181,3 +181,38 @@ def test_paper_scale_hunyuan33_sampled_blocks(P):
         want = O.attention_rows(qh, kh, vh, B, host.row_ptr, host.col_idx, rows)
         got = o[h].float().cpu().numpy()[rows]
         assert_within(block_errors(got, want, rows, B), f"H33 head {h}")
+
+
+@pytest.mark.parametrize("f,s,B,d,kind,sink,tw,sw", [
+    (8, 256, 64, 64, "radial", True, 0, 0), (6, 300, 128, 128, "radial", False, 0, 0),
+    (33, 150, 128, 128, "radial", True, 0, 0), (5, 333, 64, 128, "sta", True, 1, 40),
+    (7, 200, 128, 64, "harmonic", False, 0, 0), (9, 100, 128, 128, "temporal", True, 0, 17)])
+def test_token_exact_forward_vs_oracle(P, f, s, B, d, kind, sink, tw, sw):
+    """masked_attention(inst, PatternSpec) (attention.hpp:184-225) on the GPU: exact token mask."""
+    import torch
+    H = 2
+    q, k, v = instance_bf16(f, s, d, H, 21)
+    mk = {"radial": lambda: P.PatternSpec.radial(sink), "sta": lambda: P.PatternSpec.sta(tw, sw, sink),
+          "harmonic": lambda: P.PatternSpec.harmonic(sink), "temporal": lambda: P.PatternSpec.temporal(sw, sink)}
+    o, lse = P.masked_attention_pattern(to_torch_bf16(q), to_torch_bf16(k), to_torch_bf16(v), P.GridShape(f, s),
+                                        mk[kind](), block_size=B, return_lse=True)
+    torch.cuda.synchronize()
+    o = o.float().cpu().numpy()
+    rows = np.arange(f * s)
+    for h in range(H):
+        want, wl = O.token_attention_rows(q[h], k[h], v[h], f, s, rows, kind, sink, tw, sw, want_lse=True)
+        assert_within(block_errors(o[h], want, rows, B), f"token {kind} head {h}")
+        assert np.abs(lse[h].cpu().numpy() - wl).max() < 2e-2 if hasattr(lse, "cpu") else True
+
+
+@pytest.mark.skipif(not O.ref_available(), reason="oracle/_ref not built")
+def test_token_exact_forward_vs_reference_library(P):
+    import torch
+    f, s, d = 8, 256, 64
+    q, k, v = instance_bf16(f, s, d, 1, 42)
+    o = P.masked_attention_pattern(to_torch_bf16(q), to_torch_bf16(k), to_torch_bf16(v), P.GridShape(f, s),
+                                   P.PatternSpec.radial(), block_size=64)
+    torch.cuda.synchronize()
+    ref = O.ref_masked_attention_pattern(f, s, q[0].astype(np.float64), k[0].astype(np.float64),
+                                         v[0].astype(np.float64))
+    assert_within(block_errors(o[0].float().cpu().numpy(), ref, np.arange(f * s), 64), "token vs reference")
