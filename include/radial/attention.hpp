@@ -129,6 +129,28 @@ inline Matrix masked_attention(const AttentionInstance& inst, const BlockLayout&
     return out;
 }
 
+// radial::masked_attention(inst, PatternSpec) (attention.hpp:184-225): the token-exact
+// mask on the B200 (K2 in token mode over the pattern's 128-block layout).  Frame-structured
+// kinds only (power: invalid_argument on the device path).
+inline Matrix masked_attention(const AttentionInstance& inst, const PatternSpec& pattern) {
+    detail::check_device_instance(inst);
+    pattern.validate();
+    const std::size_t n = inst.shape.total_tokens();
+    radial_layout* h = nullptr;
+    detail::check_status(radial_cuda_mask_build(inst.shape.frames, inst.shape.tokens_per_frame, 128,
+                                                static_cast<int>(pattern.kind), pattern.sink ? 1 : 0,
+                                                pattern.temporal_window.value_or(0),
+                                                pattern.spatial_window.value_or(0), nullptr, &h));
+    detail::DeviceLayout dev(h);
+    auto q = detail::pack(inst.query), k = detail::pack(inst.key), v = detail::pack(inst.value);
+    std::vector<std::uint16_t> o(q.size());
+    detail::check_status(radial_cuda_attn_fwd_token_host(q.data(), k.data(), v.data(), o.data(), nullptr, 1, n,
+                                                         inst.head_dim, 0.f, dev.h, nullptr));
+    Matrix out(n, inst.head_dim);
+    for (std::size_t i = 0; i < o.size(); ++i) out.data[i] = detail::from_bf16(o[i]);
+    return out;
+}
+
 // radial::dense_attention (attention.hpp:141-163) on the B200 (K4 comparator).
 inline Matrix dense_attention(const AttentionInstance& inst) {
     detail::check_device_instance(inst);

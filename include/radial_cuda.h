@@ -112,6 +112,12 @@ int radial_cuda_attn_fwd_token(const void* q, const void* k, const void* v, void
                                uint32_t heads, uint64_t n, uint32_t head_dim, float scale,
                                const radial_layout* layout, void* stream);
 
+/* Host-buffer variant of radial_cuda_attn_fwd_token (masked_attention(inst, PatternSpec)'s
+ * call shape). */
+int radial_cuda_attn_fwd_token_host(const void* q, const void* k, const void* v, void* o, float* lse,
+                                    uint32_t heads, uint64_t n, uint32_t head_dim, float scale,
+                                    const radial_layout* layout, void* stream);
+
 /* ---- dense comparator: replaces radial::dense_attention (attention.hpp:141-163),
  *      same kernel over every KV block; block_size picks the KV tile (64/128). */
 int radial_cuda_attn_fwd_dense(const void* q, const void* k, const void* v, void* o, float* lse,

@@ -99,7 +99,7 @@ float resolve_scale(float scale, uint32_t D) {
 // D2H o (+ lse), synchronise.  Device workspace cached per thread and device.
 int host_fwd(const void* q, const void* k, const void* v, void* o, float* lse, uint32_t heads,
              uint64_t n, uint32_t head_dim, uint32_t BK, float scale, const radial_layout* L,
-             cudaStream_t st) {
+             cudaStream_t st, bool token = false) {
     thread_local void* ws = nullptr;
     thread_local size_t ws_bytes = 0;
     thread_local int ws_dev = -1;
@@ -126,7 +126,7 @@ int host_fwd(const void* q, const void* k, const void* v, void* o, float* lse, u
     RADIAL_CUDA_TRY(cudaMemcpyAsync(dk, k, tbytes, cudaMemcpyHostToDevice, st));
     RADIAL_CUDA_TRY(cudaMemcpyAsync(dv, v, tbytes, cudaMemcpyHostToDevice, st));
     int rc = launch_fwd(dq, dk, dv, dO, lse ? dl : nullptr, heads, n, head_dim, BK,
-                        resolve_scale(scale, head_dim), L, st);
+                        resolve_scale(scale, head_dim), L, st, token);
     if (rc) return rc;
     RADIAL_CUDA_TRY(cudaMemcpyAsync(o, dO, tbytes, cudaMemcpyDeviceToHost, st));
     if (lse) RADIAL_CUDA_TRY(cudaMemcpyAsync(lse, dl, lbytes, cudaMemcpyDeviceToHost, st));
@@ -320,6 +320,20 @@ int radial_cuda_attn_fwd_host(const void* q, const void* k, const void* v, void*
     if ((rc = check_layout_for_attn(layout, n))) return rc;
     return host_fwd(q, k, v, o, lse, heads, n, head_dim, layout->B, scale, layout,
                     static_cast<cudaStream_t>(stream));
+}
+
+int radial_cuda_attn_fwd_token_host(const void* q, const void* k, const void* v, void* o, float* lse,
+                                    uint32_t heads, uint64_t n, uint32_t head_dim, float scale,
+                                    const radial_layout* layout, void* stream) {
+    int rc = check_attn(q, k, v, o, heads, n, head_dim);
+    if (rc) return rc;
+    if ((rc = check_layout_for_attn(layout, n))) return rc;
+    if (layout->kind == RADIAL_KIND_POWER)
+        return fail(RADIAL_ERR_INVALID, "masked_attention: the power pattern has no per-frame span on the device path");
+    if (!layout->from_pattern)
+        return fail(RADIAL_ERR_INVALID, "masked_attention: token-exact mode needs a layout built by radial_cuda_mask_build");
+    return host_fwd(q, k, v, o, lse, heads, n, head_dim, layout->B, scale, layout,
+                    static_cast<cudaStream_t>(stream), true);
 }
 
 int radial_cuda_attn_fwd_dense_host(const void* q, const void* k, const void* v, void* o, float* lse,

@@ -129,6 +129,17 @@ int main() {
         report(rel < 1e-2, "masked_attention f" + std::to_string(f) + " s" + std::to_string(s) + " B" +
                                std::to_string(B) + " d" + std::to_string(d) + " rel-L2 " + std::to_string(rel));
     }
+    // token-exact masked_attention(inst, PatternSpec) vs a naive token-masked softmax
+    {
+        GridShape shape(6, 300);
+        auto inst = random_instance(shape, 128, 9);
+        auto got = masked_attention(inst, PatternSpec::radial(true));
+        // B = 1 layout == the token mask (test_blocksparse.cpp:78-90), built on the GPU
+        auto tok = blockify(shape, PatternSpec::radial(true), 1);
+        auto want = naive(inst, &tok, true);
+        const double rel = rel_l2(got, want);
+        report(rel < 1e-2, "masked_attention(inst, PatternSpec) token-exact rel-L2 " + std::to_string(rel));
+    }
     // dense_attention vs naive dense (test_attention.cpp:80-83 style)
     {
         auto inst = random_instance(GridShape(4, 100), 128, 123);
