@@ -1,6 +1,7 @@
 // radial_cuda.cu -- the C-ABI (include/radial_cuda.h): layout handles,
 // argument validation with the reference's error semantics, launches.
 #include <cstring>
+#include <new>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -96,40 +97,97 @@ float resolve_scale(float scale, uint32_t D) {
 }
 
 // Host-buffer forward: H2D q/k/v, kernel (sparse when L != nullptr, else dense),
-// D2H o (+ lse), synchronise.  Device workspace cached per thread and device.
+// D2H o (+ lse), synchronise.  Heads are processed in groups on a three-stage stream
+// pipeline -- copy-in of group g+1 and copy-out of group g-1 overlap the kernel of
+// group g (H2D and D2H use separate copy engines) -- so end-to-end time approaches
+// the kernel time plus one group's transfers.  Heads are independent, so the result
+// is identical to one monolithic call.  Device workspace and helper streams are cached
+// per thread and device.
+struct HostPipe {
+    int dev = -1;
+    void* ws = nullptr;
+    size_t ws_bytes = 0;
+    cudaStream_t in = nullptr, out = nullptr, comp[2] = {nullptr, nullptr};
+    std::vector<cudaEvent_t> ev;
+    ~HostPipe() {
+        if (ws) cudaFree(ws);
+        for (cudaStream_t s : {in, out, comp[0], comp[1]})
+            if (s) cudaStreamDestroy(s);
+        for (auto e : ev) cudaEventDestroy(e);
+    }
+};
+
 int host_fwd(const void* q, const void* k, const void* v, void* o, float* lse, uint32_t heads,
              uint64_t n, uint32_t head_dim, uint32_t BK, float scale, const radial_layout* L,
              cudaStream_t st, bool token = false) {
-    thread_local void* ws = nullptr;
-    thread_local size_t ws_bytes = 0;
-    thread_local int ws_dev = -1;
+    thread_local HostPipe hp;
     int dev = 0;
     RADIAL_CUDA_TRY(cudaGetDevice(&dev));
-    const size_t tbytes = static_cast<size_t>(heads) * n * head_dim * 2;
+    const size_t hbytes = static_cast<size_t>(n) * head_dim * 2;  // one head of one tensor
+    const size_t tbytes = hbytes * heads;
     const size_t lbytes = static_cast<size_t>(heads) * n * 4;
     const size_t need = 4 * tbytes + lbytes + 4096;
-    if (ws_bytes < need || ws_dev != dev) {
-        if (ws) cudaFree(ws);
-        ws = nullptr;
-        ws_bytes = 0;
-        RADIAL_CUDA_TRY(cudaMalloc(&ws, need));
-        ws_bytes = need;
-        ws_dev = dev;
+    if (hp.dev != dev) {
+        hp.~HostPipe();
+        new (&hp) HostPipe();
+        hp.dev = dev;
+        for (cudaStream_t* s : {&hp.in, &hp.out, &hp.comp[0], &hp.comp[1]})
+            RADIAL_CUDA_TRY(cudaStreamCreateWithFlags(s, cudaStreamNonBlocking));
     }
-    auto* base = static_cast<uint8_t*>(ws);
-    void* dq = base;
-    void* dk = base + tbytes;
-    void* dv = base + 2 * tbytes;
-    void* dO = base + 3 * tbytes;
+    if (hp.ws_bytes < need) {
+        if (hp.ws) cudaFree(hp.ws);
+        hp.ws = nullptr;
+        hp.ws_bytes = 0;
+        RADIAL_CUDA_TRY(cudaMalloc(&hp.ws, need));
+        hp.ws_bytes = need;
+    }
+    auto* base = static_cast<uint8_t*>(hp.ws);
+    auto* dq = base;
+    auto* dk = base + tbytes;
+    auto* dv = base + 2 * tbytes;
+    auto* dO = base + 3 * tbytes;
     float* dl = reinterpret_cast<float*>(base + 4 * tbytes);
-    RADIAL_CUDA_TRY(cudaMemcpyAsync(dq, q, tbytes, cudaMemcpyHostToDevice, st));
-    RADIAL_CUDA_TRY(cudaMemcpyAsync(dk, k, tbytes, cudaMemcpyHostToDevice, st));
-    RADIAL_CUDA_TRY(cudaMemcpyAsync(dv, v, tbytes, cudaMemcpyHostToDevice, st));
-    int rc = launch_fwd(dq, dk, dv, dO, lse ? dl : nullptr, heads, n, head_dim, BK,
-                        resolve_scale(scale, head_dim), L, st, token);
-    if (rc) return rc;
-    RADIAL_CUDA_TRY(cudaMemcpyAsync(o, dO, tbytes, cudaMemcpyDeviceToHost, st));
-    if (lse) RADIAL_CUDA_TRY(cudaMemcpyAsync(lse, dl, lbytes, cudaMemcpyDeviceToHost, st));
+    // group size: ~6 groups (first-group latency vs per-kernel tail), at least 1 head
+    const uint32_t gh = std::max<uint32_t>(1, (heads + 5) / 6);
+    const uint32_t groups = (heads + gh - 1) / gh;
+    while (hp.ev.size() < 3 * static_cast<size_t>(groups) + 1) {
+        cudaEvent_t e;
+        RADIAL_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        hp.ev.push_back(e);
+    }
+    cudaEvent_t start = hp.ev[3 * groups];
+    RADIAL_CUDA_TRY(cudaEventRecord(start, st));  // order after prior work on the caller's stream
+    RADIAL_CUDA_TRY(cudaStreamWaitEvent(hp.in, start, 0));
+    const float sc = resolve_scale(scale, head_dim);
+    for (uint32_t g = 0; g < groups; ++g) {
+        const uint32_t h0 = g * gh, hn = std::min(gh, heads - h0);
+        const size_t off = hbytes * h0, len = hbytes * hn;
+        cudaEvent_t e_in = hp.ev[3 * g], e_k = hp.ev[3 * g + 1], e_out = hp.ev[3 * g + 2];
+        const auto* hq = static_cast<const uint8_t*>(q) + off;
+        const auto* hk = static_cast<const uint8_t*>(k) + off;
+        const auto* hv = static_cast<const uint8_t*>(v) + off;
+        RADIAL_CUDA_TRY(cudaMemcpyAsync(dq + off, hq, len, cudaMemcpyHostToDevice, hp.in));
+        RADIAL_CUDA_TRY(cudaMemcpyAsync(dk + off, hk, len, cudaMemcpyHostToDevice, hp.in));
+        RADIAL_CUDA_TRY(cudaMemcpyAsync(dv + off, hv, len, cudaMemcpyHostToDevice, hp.in));
+        RADIAL_CUDA_TRY(cudaEventRecord(e_in, hp.in));
+        cudaStream_t cs = hp.comp[g & 1];  // alternate so one group's tail overlaps the next
+        RADIAL_CUDA_TRY(cudaStreamWaitEvent(cs, e_in, 0));
+        int rc = launch_fwd(dq + off, dk + off, dv + off, dO + off,
+                            lse ? dl + static_cast<size_t>(h0) * n : nullptr, hn, n, head_dim, BK, sc, L, cs,
+                            token);
+        if (rc) return rc;
+        RADIAL_CUDA_TRY(cudaEventRecord(e_k, cs));
+        RADIAL_CUDA_TRY(cudaStreamWaitEvent(hp.out, e_k, 0));
+        RADIAL_CUDA_TRY(cudaMemcpyAsync(static_cast<uint8_t*>(o) + off, dO + off, len, cudaMemcpyDeviceToHost,
+                                        hp.out));
+        if (lse)
+            RADIAL_CUDA_TRY(cudaMemcpyAsync(lse + static_cast<size_t>(h0) * n, dl + static_cast<size_t>(h0) * n,
+                                            static_cast<size_t>(hn) * n * 4, cudaMemcpyDeviceToHost, hp.out));
+        RADIAL_CUDA_TRY(cudaEventRecord(e_out, hp.out));
+    }
+    // the caller's stream sees the whole call complete (events timed on it bracket it)
+    RADIAL_CUDA_TRY(cudaStreamWaitEvent(st, hp.ev[3 * (groups - 1) + 2], 0));
+    (void)lbytes;
     RADIAL_CUDA_TRY(cudaStreamSynchronize(st));
     return RADIAL_OK;
 }
