@@ -30,6 +30,19 @@ int make_tmap_bf16_3d(CUtensorMap* m, const void* base, uint64_t n, uint32_t D, 
                       uint32_t box_rows);
 }
 
+#ifdef RADIAL_TRACE
+__device__ unsigned long long* g_btrace = nullptr;
+#define BTRACE(ev, j)                                                                         \
+    do {                                                                                      \
+        if (g_btrace && blockIdx.x < 4 && (j) < 64)                                           \
+            g_btrace[(blockIdx.x * 64 + (j)) * 16 + (ev)] = clock64();                       \
+    } while (0)
+#else
+#define BTRACE(ev, j) \
+    do {              \
+    } while (0)
+#endif
+
 namespace {
 
 constexpr int kThreads = 384;   // warp0 TMA, warp1 MMA, warp2 TMEM alloc, warps 4-11 elementwise
@@ -171,10 +184,13 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint32_t kv0 = smem_u32(smem + 2 * T);
             uint32_t dsph[2] = {0, 0};
             bool acc = false;
+            uint32_t dq_j = 0;  // block index of the dS being consumed (trace only)
+            (void)dq_j;
             // dQ += dS(sub-buffer b) . K(rows of that sub-step)
             auto dq_mma = [&](auto BC, uint32_t k_tile) {
                 constexpr int b = decltype(BC)::value;
                 mbar_wait(&bar_ds[b], dsph[b]);
+                BTRACE(3 + b, dq_j);
                 dsph[b] ^= 1;
                 tc_fence_after();
 #pragma unroll
@@ -188,6 +204,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const uint32_t k_s = kv0 + st * 2 * T, v_s = k_s + T;
                 const uint32_t k_prev = kv0 + (st ^ 1) * 2 * T;
                 mbar_wait(&bar_full[st], (j >> 1) & 1);
+                BTRACE(0, j);
                 tc_fence_after();
                 auto sub = [&](auto BC) {
                     constexpr int b = decltype(BC)::value;
@@ -200,13 +217,16 @@ __global__ void __launch_bounds__(kThreads, 1)
                         mma_ss(kTmem + 128 + b * 64, kdesc(do_s, kk, 0), kdesc(v_s, kk, b * kSub), Cfg::kIdS,
                                kk ? 1u : 0u);
                     mma_commit(&bar_s[b]);
+                    BTRACE(1 + b, j);
                 };
                 sub(std::integral_constant<int, 0>{});
                 if (j > 0) {  // previous block's second sub-step, then free its K/V stage
+                    dq_j = j - 1;
                     dq_mma(std::integral_constant<int, 1>{}, k_prev);
                     mma_commit(&bar_empty[st ^ 1]);
                 }
                 sub(std::integral_constant<int, 1>{});
+                dq_j = j;
                 dq_mma(std::integral_constant<int, 0>{}, k_s);
             }
             if (L > 0) dq_mma(std::integral_constant<int, 1>{}, kv0 + ((L - 1) & 1) * 2 * T);
@@ -225,7 +245,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         const float sl2 = p.scale_log2;
         for (uint32_t j = 0; j < L; ++j) {
             const uint32_t J = __ldg(p.idx + e0 + j);
+            if ((warp & 3) == 0 && lane == 0) BTRACE(5 + 2 * wg, j);
             mbar_wait(&bar_s[wg], j & 1);
+            if ((warp & 3) == 0 && lane == 0) BTRACE(5 + 2 * wg, j);
             tc_fence_after();
             uint32_t sv[64], dp[64];
             tmem_ld32(kTmem + la + wg * 64, *reinterpret_cast<uint32_t(*)[32]>(sv));
@@ -254,6 +276,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&bar_ds[wg]);
+            if ((warp & 3) == 0 && lane == 0) BTRACE(6 + 2 * wg, j);
         }
         // ---------------------------------------------------- epilogue: dQ * scale
         mbar_wait(bar_acc, 0);
@@ -562,5 +585,12 @@ int launch_bwd(const void* q, const void* k, const void* v, const void* o, const
     if (D == 64) return launch_bwd_t<64>(q, k, v, o, lse, dout, dq, dk, dv, heads, n, scale, L, workspace, st);
     return fail(RADIAL_ERR_INVALID, "attn_bwd: head_dim must be 64 or 128");
 }
+
+#ifdef RADIAL_TRACE
+extern "C" int radial_cuda_debug_btrace(void* buf) {
+    RADIAL_CUDA_TRY(cudaMemcpyToSymbol(g_btrace, &buf, sizeof(void*)));
+    return RADIAL_OK;
+}
+#endif
 
 }  // namespace radial_detail

@@ -531,7 +531,9 @@ int launch_fwd_t(const void* q, const void* k, const void* v, void* o, float* ls
     if (L) {
         p.uptr = L->uptr;
         p.uidx = L->uidx;
+#ifndef RADIAL_FWD_NATURAL_ORDER
         p.order = L->uorder;
+#endif
     }
     if (token) {
         p.rule = radial_rule::MaskParams{L->f, L->s, L->B, n, L->kind, L->sink, L->tw, L->sw};
