@@ -101,6 +101,16 @@ struct BwdCfg {
     static constexpr uint32_t kIdAcc = idesc_bf16(128, D, 0, 1);   // 128 x D x 16, B MN-major
 };
 
+// Base descriptors: an MMA's descriptor = base + (byte offset >> 4); the 14-bit start
+// address field never carries (all offsets stay inside the 227 KB of shared memory).
+// Keeping every offset a compile-time constant keeps the tcgen05 operands uniform.
+__device__ __forceinline__ uint64_t kbase(uint32_t smem_addr) { return sdesc_sw128(smem_addr, 16, 1024); }
+__device__ __forceinline__ uint64_t mnbase(uint32_t smem_addr) { return sdesc_sw128(smem_addr, kBlk * 128, 1024); }
+__host__ __device__ constexpr uint32_t koff(int kk, int row0) {
+    return static_cast<uint32_t>(((kk >> 2) * (kBlk * 128) + row0 * 128 + (kk & 3) * 32) >> 4);
+}
+__host__ __device__ constexpr uint32_t mnoff(int row0) { return static_cast<uint32_t>((row0 * 128) >> 4); }
+
 // K-major descriptor of MMA k-step kk (16 elements of d) for a 128-row tile,
 // optionally starting at row `row0` (multiple of 8).
 __device__ __forceinline__ uint64_t kdesc(uint32_t tile, int kk, int row0) {
@@ -180,56 +190,71 @@ __global__ void __launch_bounds__(kThreads, 1)
             // ------------------------------------------------ MMA issuer
             mbar_wait(bar_res, 0);
             tc_fence_after();
-            const uint32_t q_s = smem_u32(smem), do_s = smem_u32(smem + T);
-            const uint32_t kv0 = smem_u32(smem + 2 * T);
-            uint32_t dsph[2] = {0, 0};
+            const uint64_t dq_k = kbase(smem_u32(smem));          // Q (resident)
+            const uint64_t ddo_k = kbase(smem_u32(smem + T));     // dO (resident)
+            const uint64_t dkv_k = kbase(smem_u32(smem + 2 * T));  // K/V stages, K-major view
+            const uint64_t dkv_mn = mnbase(smem_u32(smem + 2 * T));  // K/V stages, MN-major view
+            uint32_t dsph0 = 0, dsph1 = 0;
             bool acc = false;
             uint32_t dq_j = 0;  // block index of the dS being consumed (trace only)
             (void)dq_j;
-            // dQ += dS(sub-buffer b) . K(rows of that sub-step)
-            auto dq_mma = [&](auto BC, uint32_t k_tile) {
+            // dQ += dS(sub-buffer b) . K(rows of that sub-step), K in stage STG
+            auto dq_mma = [&](auto BC, auto SC) {
                 constexpr int b = decltype(BC)::value;
-                mbar_wait(&bar_ds[b], dsph[b]);
+                constexpr int STG = decltype(SC)::value;
+                uint32_t& ph = b ? dsph1 : dsph0;
+                mbar_wait(&bar_ds[b], ph);
                 BTRACE(3 + b, dq_j);
-                dsph[b] ^= 1;
+                ph ^= 1;
                 tc_fence_after();
-#pragma unroll
-                for (int kk = 0; kk < kSub / 16; ++kk)
-                    mma_ts(kTmem + 256, kTmem + b * 64 + kk * 8, mndesc(k_tile, b * kSub + kk * 16),
-                           Cfg::kIdAcc, (acc || kk) ? 1u : 0u);
+                static_for<kSub / 16>([&](auto KK) {
+                    constexpr int kk = decltype(KK)::value;
+                    mma_ts_off<((STG * 2 * T) >> 4) + mnoff(b * kSub + kk * 16)>(
+                        kTmem + 256, kTmem + b * 64 + kk * 8, dkv_mn, Cfg::kIdAcc, (acc || kk) ? 1u : 0u);
+                });
                 acc = true;
             };
-            for (uint32_t j = 0; j < L; ++j) {
-                const int st = j & 1;
-                const uint32_t k_s = kv0 + st * 2 * T, v_s = k_s + T;
-                const uint32_t k_prev = kv0 + (st ^ 1) * 2 * T;
-                mbar_wait(&bar_full[st], (j >> 1) & 1);
+            auto block = [&](uint32_t j, auto SC) {
+                constexpr int STG = decltype(SC)::value;  // == j % 2
+                mbar_wait(&bar_full[STG], (j >> 1) & 1);
                 BTRACE(0, j);
                 tc_fence_after();
                 auto sub = [&](auto BC) {
                     constexpr int b = decltype(BC)::value;
                     // S_b = Q K_sub^T ; dP_b = dO V_sub^T   (128 x 64, K = d)
-#pragma unroll
-                    for (int kk = 0; kk < D / 16; ++kk)
-                        mma_ss(kTmem + b * 64, kdesc(q_s, kk, 0), kdesc(k_s, kk, b * kSub), Cfg::kIdS, kk ? 1u : 0u);
-#pragma unroll
-                    for (int kk = 0; kk < D / 16; ++kk)
-                        mma_ss(kTmem + 128 + b * 64, kdesc(do_s, kk, 0), kdesc(v_s, kk, b * kSub), Cfg::kIdS,
-                               kk ? 1u : 0u);
+                    static_for<D / 16>([&](auto KK) {
+                        constexpr int kk = decltype(KK)::value;
+                        mma_ss_off<koff(kk, 0), ((STG * 2 * T) >> 4) + koff(kk, b * kSub)>(
+                            kTmem + b * 64, dq_k, dkv_k, Cfg::kIdS, kk ? 1u : 0u);
+                    });
+                    static_for<D / 16>([&](auto KK) {
+                        constexpr int kk = decltype(KK)::value;
+                        mma_ss_off<koff(kk, 0), ((STG * 2 * T + T) >> 4) + koff(kk, b * kSub)>(
+                            kTmem + 128 + b * 64, ddo_k, dkv_k, Cfg::kIdS, kk ? 1u : 0u);
+                    });
                     mma_commit(&bar_s[b]);
                     BTRACE(1 + b, j);
                 };
                 sub(std::integral_constant<int, 0>{});
                 if (j > 0) {  // previous block's second sub-step, then free its K/V stage
                     dq_j = j - 1;
-                    dq_mma(std::integral_constant<int, 1>{}, k_prev);
-                    mma_commit(&bar_empty[st ^ 1]);
+                    dq_mma(std::integral_constant<int, 1>{}, std::integral_constant<int, STG ^ 1>{});
+                    mma_commit(&bar_empty[STG ^ 1]);
                 }
                 sub(std::integral_constant<int, 1>{});
                 dq_j = j;
-                dq_mma(std::integral_constant<int, 0>{}, k_s);
+                dq_mma(std::integral_constant<int, 0>{}, std::integral_constant<int, STG>{});
+            };
+            for (uint32_t j = 0; j < L; j += 2) {
+                block(j, std::integral_constant<int, 0>{});
+                if (j + 1 < L) block(j + 1, std::integral_constant<int, 1>{});
             }
-            if (L > 0) dq_mma(std::integral_constant<int, 1>{}, kv0 + ((L - 1) & 1) * 2 * T);
+            if (L > 0) {
+                if ((L - 1) & 1)
+                    dq_mma(std::integral_constant<int, 1>{}, std::integral_constant<int, 1>{});
+                else
+                    dq_mma(std::integral_constant<int, 1>{}, std::integral_constant<int, 0>{});
+            }
             mma_commit(bar_acc);
         }
     } else {
