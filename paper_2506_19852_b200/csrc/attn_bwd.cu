@@ -52,6 +52,8 @@ constexpr uint32_t kTmem = 0;   // whole-SM TMEM allocation starts at column 0
 constexpr float kLog2e = 1.4426950408889634f;
 
 struct BwdParams {
+    const __nv_bfloat16* q;     // dQ kernel: Q and dO rows go straight to TMEM
+    const __nv_bfloat16* dout;
     __nv_bfloat16* dq;
     __nv_bfloat16* dk;
     __nv_bfloat16* dv;
@@ -122,7 +124,8 @@ __device__ __forceinline__ uint64_t mndesc(uint32_t tile, int row0) {
 }
 
 // ============================================================================ dQ
-// TMEM: S0 [0,64) S1 [64,128) dP0 [128,192) dP1 [192,256) dQ [256,256+D)
+// TMEM: S0 [0,64) S1 [64,128) dP0 [128,192) dP1 [192,256) dQ [256,256+D) Q [384,448) dO [448,512)
+constexpr uint32_t kColQ = 384, kColDO = 448;
 template <int D>
 __global__ void __launch_bounds__(kThreads, 1)
     radial_attn_bwd_dq_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_do,
@@ -150,7 +153,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t L = static_cast<uint32_t>(p.ptr[I + 1] - e0);
 
     if (warp == 0 && lane == 0) {
-        mbar_init(bar_res, 1);
+        mbar_init(bar_res, 8);  // Q / dO rows stored into TMEM by the 8 elementwise warps
         for (int i = 0; i < 2; ++i) {
             mbar_init(&bar_full[i], 1);
             mbar_init(&bar_empty[i], 1);
@@ -170,11 +173,6 @@ __global__ void __launch_bounds__(kThreads, 1)
         regs_dec<104>();
         if (warp == 0 && lane == 0) {
             // ------------------------------------------------ producer
-            mbar_arrive_expect_tx(bar_res, 2 * T);
-            for (int a = 0; a < Cfg::kAtoms; ++a) {
-                tma_load_3d(smem + a * Cfg::kAtomBytes, &tm_q, bar_res, a * 64, I * kBlk, head);
-                tma_load_3d(smem + T + a * Cfg::kAtomBytes, &tm_do, bar_res, a * 64, I * kBlk, head);
-            }
             for (uint32_t j = 0; j < L; ++j) {
                 const int st = j & 1;
                 const int32_t J = static_cast<int32_t>(__ldg(p.idx + e0 + j));
@@ -190,8 +188,6 @@ __global__ void __launch_bounds__(kThreads, 1)
             // ------------------------------------------------ MMA issuer
             mbar_wait(bar_res, 0);
             tc_fence_after();
-            const uint64_t dq_k = kbase(smem_u32(smem));          // Q (resident)
-            const uint64_t ddo_k = kbase(smem_u32(smem + T));     // dO (resident)
             const uint64_t dkv_k = kbase(smem_u32(smem + 2 * T));  // K/V stages, K-major view
             const uint64_t dkv_mn = mnbase(smem_u32(smem + 2 * T));  // K/V stages, MN-major view
             uint32_t dsph0 = 0, dsph1 = 0;
@@ -221,16 +217,18 @@ __global__ void __launch_bounds__(kThreads, 1)
                 tc_fence_after();
                 auto sub = [&](auto BC) {
                     constexpr int b = decltype(BC)::value;
-                    // S_b = Q K_sub^T ; dP_b = dO V_sub^T   (128 x 64, K = d)
+                    // S_b = Q K_sub^T ; dP_b = dO V_sub^T   (128 x 64, K = d): TS MMAs with
+                    // Q / dO read from TMEM, so only the 64-row K / V sub-tile streams from
+                    // shared memory (an SS MMA at N = 64 is shared-memory bound)
                     static_for<D / 16>([&](auto KK) {
                         constexpr int kk = decltype(KK)::value;
-                        mma_ss_off<koff(kk, 0), ((STG * 2 * T) >> 4) + koff(kk, b * kSub)>(
-                            kTmem + b * 64, dq_k, dkv_k, Cfg::kIdS, kk ? 1u : 0u);
+                        mma_ts_off<((STG * 2 * T) >> 4) + koff(kk, b * kSub)>(
+                            kTmem + b * 64, kTmem + kColQ + kk * 8, dkv_k, Cfg::kIdS, kk ? 1u : 0u);
                     });
                     static_for<D / 16>([&](auto KK) {
                         constexpr int kk = decltype(KK)::value;
-                        mma_ss_off<koff(kk, 0), ((STG * 2 * T + T) >> 4) + koff(kk, b * kSub)>(
-                            kTmem + 128 + b * 64, ddo_k, dkv_k, Cfg::kIdS, kk ? 1u : 0u);
+                        mma_ts_off<((STG * 2 * T + T) >> 4) + koff(kk, b * kSub)>(
+                            kTmem + 128 + b * 64, kTmem + kColDO + kk * 8, dkv_k, Cfg::kIdS, kk ? 1u : 0u);
                     });
                     mma_commit(&bar_s[b]);
                     BTRACE(1 + b, j);
@@ -265,6 +263,35 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t la = static_cast<uint32_t>((warp & 3) * 32) << 16;
         const uint64_t row = static_cast<uint64_t>(I) * kBlk + r;
         const uint64_t prow = static_cast<uint64_t>(head) * p.rpad + row;
+        {
+            // resident A operands: warpgroup 0 stores this row of Q, warpgroup 1 of dO, as
+            // packed bf16 pairs in TMEM (lane = row, column c = elements 2c, 2c+1)
+            const __nv_bfloat16* src = (wg ? p.dout : p.q) + (static_cast<uint64_t>(head) * p.n + row) * D;
+            const uint32_t col = wg ? kColDO : kColQ;
+#pragma unroll
+            for (int c = 0; c < D / 2; c += 16) {
+                uint32_t w[16];
+                if (row < p.n) {
+                    const uint4* g = reinterpret_cast<const uint4*>(src + 2 * c);
+#pragma unroll
+                    for (int x = 0; x < 4; ++x) {
+                        const uint4 u = __ldg(g + x);
+                        w[4 * x] = u.x;
+                        w[4 * x + 1] = u.y;
+                        w[4 * x + 2] = u.z;
+                        w[4 * x + 3] = u.w;
+                    }
+                } else {
+#pragma unroll
+                    for (int x = 0; x < 16; ++x) w[x] = 0u;
+                }
+                tmem_st16(kTmem + la + col + c, w);
+            }
+            tmem_wait_st();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(bar_res);
+        }
         const float lse2 = p.lse2[prow];
         const float dval = p.dvec[prow];
         const float sl2 = p.scale_log2;
@@ -553,6 +580,8 @@ int launch_bwd_t(const void* q, const void* k, const void* v, const void* o, con
     if ((rc = make_tmap_bf16_3d(&tk, k, n, D, heads, kBlk))) return rc;
     if ((rc = make_tmap_bf16_3d(&tv, v, n, D, heads, kBlk))) return rc;
     BwdParams p{};
+    p.q = static_cast<const __nv_bfloat16*>(q);
+    p.dout = static_cast<const __nv_bfloat16*>(dout);
     p.dq = static_cast<__nv_bfloat16*>(dq);
     p.dk = static_cast<__nv_bfloat16*>(dk);
     p.dv = static_cast<__nv_bfloat16*>(dv);
