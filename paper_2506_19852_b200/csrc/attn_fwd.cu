@@ -11,7 +11,7 @@
 // blocks it does not keep, so FLOPs are exactly the kept blocks.
 //
 // Warp roles (384 threads, one CTA per SM):
-//   warp 0      TMA producer: Q tiles once, then K_j / V_j into 2-stage rings
+//   warp 0      TMA producer: Q tiles once, then K_j, V_j into one 5-slot ring
 //   warp 1      MMA issuer (one thread): S_t = Q_t K_j^T (SS, both operands
 //               K-major in smem) and O_t += P_t V_j (TS: P from TMEM, V
 //               MN-major in smem), tcgen05.commit -> mbarriers
@@ -34,7 +34,7 @@ using namespace radial_sm100;
 // Debug-only event trace (compile with -DRADIAL_TRACE): SM clock stamps for the
 // first kTraceCtas CTAs, kTraceEv events per KV step.
 __device__ unsigned long long* g_trace = nullptr;
-constexpr int kTraceCtas = 4, kTraceSteps = 64, kTraceEv = 16;
+constexpr int kTraceCtas = 4, kTraceSteps = 64, kTraceEv = 24;
 #define TRACE(ev, j)                                                                         \
     do {                                                                                     \
         if (g_trace && blockIdx.x < kTraceCtas && (j) < kTraceSteps)                          \
@@ -51,8 +51,11 @@ namespace {
 constexpr int kThreads = 384;
 constexpr uint32_t kTmem = 0;   // TMEM base address (checked against tcgen05.alloc)
 constexpr int kBQ = 128;        // query rows per tile
-constexpr int kStagesK = 2;   // the MMA loop is unrolled by the ring depth (2)
-constexpr int kStagesV = 2;
+// K_j and V_j share one ring of kSlots tiles, in load order K0 V0 K1 V1 ...: tile t = 2j
+// (K_j) or 2j + 1 (V_j) lives in slot t % kSlots.  The MMA issue order frees them in the
+// same order (K_j after S_B(j), V_j after PV_B(j)), so one ring suffices and every tile
+// is prefetched kSlots / 2 steps ahead (the L2 -> SM latency under load is ~1 step).
+constexpr int kSlots = 5;  // the MMA loop is unrolled by kSlots steps (constant slot indices)
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
 #ifndef RADIAL_POLY_PAIRS
 #define RADIAL_POLY_PAIRS 0  // measured on B200: MUFU-only is fastest with the current pipeline
@@ -82,10 +85,9 @@ struct FwdCfg {
     static constexpr int kQBytes = kBQ * D * 2;
     static constexpr int kKVBytes = BK * D * 2;
     static constexpr int kSmemQ = 0;
-    static constexpr int kSmemK = kSmemQ + 2 * kQBytes;
-    static constexpr int kSmemV = kSmemK + kStagesK * kKVBytes;
-    static constexpr int kSmemBar = kSmemV + kStagesV * kKVBytes;
-    static constexpr int kNumBars = 1 + 2 * kStagesK + 2 * kStagesV + 2 + 4 + 2;
+    static constexpr int kSmemKV = kSmemQ + 2 * kQBytes;          // unified K/V ring
+    static constexpr int kSmemBar = kSmemKV + kSlots * kKVBytes;
+    static constexpr int kNumBars = 1 + 2 * kSlots + 2 + 4 + 2;
     static constexpr int kSmemBytes = kSmemBar + kNumBars * 8 + 16;
     static constexpr int kSmemAlloc = kSmemBytes + 1024;  // slack for 1024 B alignment
     // TMEM columns
@@ -106,11 +108,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                                                ~static_cast<uintptr_t>(1023));
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Cfg::kSmemBar);
     uint64_t* bar_q = bars;
-    uint64_t* bar_kfull = bars + 1;
-    uint64_t* bar_kempty = bar_kfull + kStagesK;
-    uint64_t* bar_vfull = bar_kempty + kStagesK;
-    uint64_t* bar_vempty = bar_vfull + kStagesV;
-    uint64_t* bar_sfull = bar_vempty + kStagesV;  // [2]
+    uint64_t* bar_full = bars + 1;
+    uint64_t* bar_empty = bar_full + kSlots;
+    uint64_t* bar_sfull = bar_empty + kSlots;  // [2]
     uint64_t* bar_pready = bar_sfull + 2;          // [2 tiles][2 key halves]
     uint64_t* bar_ofull = bar_pready + 4;          // [2]
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar_ofull + 2);
@@ -142,13 +142,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     if (warp == 0 && lane == 0) {
         mbar_init(bar_q, 1);
-        for (int s = 0; s < kStagesK; ++s) {
-            mbar_init(&bar_kfull[s], 1);
-            mbar_init(&bar_kempty[s], 1);
-        }
-        for (int s = 0; s < kStagesV; ++s) {
-            mbar_init(&bar_vfull[s], 1);
-            mbar_init(&bar_vempty[s], 1);
+        for (int s = 0; s < kSlots; ++s) {
+            mbar_init(&bar_full[s], 1);
+            mbar_init(&bar_empty[s], 1);
         }
         for (int t = 0; t < 2; ++t) {
             mbar_init(&bar_sfull[t], 1);
@@ -181,19 +177,23 @@ __global__ void __launch_bounds__(kThreads, 1)
                 for (int a = 0; a < Cfg::kAtoms; ++a)
                     tma_load_3d(smem + Cfg::kSmemQ + t * Cfg::kQBytes + a * Cfg::kQAtomBytes, &tm_q,
                                 bar_q, a * 64, static_cast<int32_t>(row0 + t * kBQ), head);
-            for (uint32_t j = 0; j < L; ++j) {
-                const int32_t J = static_cast<int32_t>(entry(j) & 0x0FFFFFFFu);
-                const int ks = j % kStagesK, vs = j % kStagesV;
-                mbar_wait(&bar_kempty[ks], ((j / kStagesK) & 1) ^ 1);
-                mbar_arrive_expect_tx(&bar_kfull[ks], Cfg::kKVBytes);
-                uint8_t* kd = smem + Cfg::kSmemK + ks * Cfg::kKVBytes;
+            for (uint32_t t = 0; t < 2 * L; ++t) {
+                const int32_t J = static_cast<int32_t>(entry(t >> 1) & 0x0FFFFFFFu);
+                const uint32_t slot = t % kSlots;
+                mbar_wait(&bar_empty[slot], ((t / kSlots) & 1) ^ 1);
+                TRACE(18 + (t & 1), t >> 1);
+#ifdef RADIAL_SKIP_LOADS  // timing experiment only: 1 = no V loads, 2 = no K/V loads after the first ring
+                if (((RADIAL_SKIP_LOADS & 1) && (t & 1) && t >= 2 * kSlots) ||
+                    ((RADIAL_SKIP_LOADS & 2) && t >= 2 * kSlots)) {
+                    mbar_arrive(&bar_full[slot]);
+                    continue;
+                }
+#endif
+                mbar_arrive_expect_tx(&bar_full[slot], Cfg::kKVBytes);
+                uint8_t* dst = smem + Cfg::kSmemKV + slot * Cfg::kKVBytes;
+                const CUtensorMap* tm = (t & 1) ? &tm_v : &tm_k;
                 for (int a = 0; a < Cfg::kAtoms; ++a)
-                    tma_load_3d(kd + a * Cfg::kKVAtomBytes, &tm_k, &bar_kfull[ks], a * 64, J * BK, head);
-                mbar_wait(&bar_vempty[vs], ((j / kStagesV) & 1) ^ 1);
-                mbar_arrive_expect_tx(&bar_vfull[vs], Cfg::kKVBytes);
-                uint8_t* vd = smem + Cfg::kSmemV + vs * Cfg::kKVBytes;
-                for (int a = 0; a < Cfg::kAtoms; ++a)
-                    tma_load_3d(vd + a * Cfg::kKVAtomBytes, &tm_v, &bar_vfull[vs], a * 64, J * BK, head);
+                    tma_load_3d(dst + a * Cfg::kKVAtomBytes, tm, &bar_full[slot], a * 64, J * BK, head);
             }
         }
     } else if (warp == 1) {
@@ -209,59 +209,78 @@ __global__ void __launch_bounds__(kThreads, 1)
             // base descriptors; an MMA's descriptor = base + (byte offset >> 4) (the 14-bit
             // start-address field cannot carry: every offset stays inside 256 KB)
             const uint64_t dq = sdesc_sw128(smem_u32(smem + Cfg::kSmemQ), 16, 1024);
-            const uint64_t dk = sdesc_sw128(smem_u32(smem + Cfg::kSmemK), 16, 1024);
-            const uint64_t dv = sdesc_sw128(smem_u32(smem + Cfg::kSmemV), Cfg::kKVAtomBytes, 1024);
+            const uint64_t dk = sdesc_sw128(smem_u32(smem + Cfg::kSmemKV), 16, 1024);
+            const uint64_t dv = sdesc_sw128(smem_u32(smem + Cfg::kSmemKV), Cfg::kKVAtomBytes, 1024);
             bool pend0 = false, pend1 = false;
             uint32_t acc0 = 0, acc1 = 0;
             uint32_t pphase0 = 0, pphase1 = 0;
-            auto step = [&](uint32_t j, auto KSC) {
-                constexpr int KS = decltype(KSC)::value;  // == j % 2 (K ring and V ring)
-                constexpr int VSP = KS ^ 1;               // V stage of step j-1
+            uint32_t e_next = L > 0 ? entry(0) : 0u;
+            // step j: PV_A(j-1), S_A(j), PV_B(j-1), S_B(j); each operand is waited for just
+            // before its first use and released right after its last use.
+            auto step = [&](uint32_t j, auto PC) {
+                constexpr int PH = decltype(PC)::value;        // == j % kSlots
+                constexpr int KSL = (2 * PH) % kSlots;          // slot of K_j
+                constexpr int VSL = (2 * PH + kSlots - 1) % kSlots;  // slot of V_{j-1}
                 uint32_t tf0 = 0, tf1 = 0;
                 if (j < L) {
-                    const uint32_t m = entry(j) >> 28;
+                    const uint32_t m = e_next >> 28;  // entry(j), loaded one step ahead
+                    if (j + 1 < L) e_next = entry(j + 1);
                     tf0 = m & ((1u << Cfg::GT) - 1);
                     tf1 = (m >> Cfg::GT) & ((1u << Cfg::GT) - 1);
-                    mbar_wait(&bar_kfull[KS], (j >> 1) & 1);
                 }
-                if (j > 0 && (pend0 || pend1)) mbar_wait(&bar_vfull[VSP], ((j - 1) >> 1) & 1);
+                // every union entry keeps a block of at least one tile, so V_{j-1} is always
+                // consumed; it is waited for and released unconditionally (no TMA in flight
+                // into a released slot)
+                if (j > 0) mbar_wait(&bar_full[VSL], ((2 * j - 1) / kSlots) & 1);
+                TRACE(17, j);
                 tc_fence_after();
                 auto pv = [&](auto TC, uint32_t& acc, uint32_t& pphase) {
                     constexpr int T = decltype(TC)::value;
+#ifdef RADIAL_LOAD_ONLY  // timing experiment only: K/V streaming without MMAs or softmax
+                    return;
+#endif
                     constexpr uint32_t p_col = T ? Cfg::kColS1 : Cfg::kColS0;
                     constexpr uint32_t o_col = T ? Cfg::kColO1 : Cfg::kColO0;
 
-#pragma unroll
-                    for (int h = 0; h < 2; ++h) {
+                    static_for<2>([&](auto HC) {
+                        constexpr int h = decltype(HC)::value;
                         mbar_wait(&bar_pready[2 * T + h], pphase);
                         TRACE(8 + 2 * T + h, j - 1);
                         tc_fence_after();
-#pragma unroll
-                        for (int kk = h * (BK / 32); kk < (h + 1) * (BK / 32); ++kk)
-                            mma_ts(kTmem + o_col, kTmem + p_col + kk * 8,
-                                   dv + ((VSP * Cfg::kKVBytes + kk * 16 * 128) >> 4), Cfg::kIdescO,
-                                   (acc | kk) ? 1u : 0u);
-                    }
+                        static_for<BK / 32>([&](auto KI) {
+                            constexpr int kk = h * (BK / 32) + decltype(KI)::value;
+                            mma_ts_off<((VSL * Cfg::kKVBytes + kk * 16 * 128) >> 4)>(
+                                kTmem + o_col, kTmem + p_col + kk * 8, dv, Cfg::kIdescO, (acc | kk) ? 1u : 0u);
+                        });
+                    });
                     pphase ^= 1;
                     acc = 1;
                 };
                 auto qk = [&](auto TC) {
                     constexpr int T = decltype(TC)::value;
+#ifdef RADIAL_LOAD_ONLY
+                    return;
+#endif
                     constexpr uint32_t s_col = T ? Cfg::kColS1 : Cfg::kColS0;
 
-#pragma unroll
-                    for (int kk = 0; kk < D / 16; ++kk) {
-                        const uint32_t off_q = (kk >> 2) * Cfg::kQAtomBytes + (kk & 3) * 32;
-                        const uint32_t off_k = (kk >> 2) * Cfg::kKVAtomBytes + (kk & 3) * 32;
-                        mma_ss(kTmem + s_col, dq + ((T * Cfg::kQBytes + off_q) >> 4),
-                               dk + ((KS * Cfg::kKVBytes + off_k) >> 4), Cfg::kIdescS, kk ? 1u : 0u);
-                    }
+                    static_for<D / 16>([&](auto KC) {
+                        constexpr int kk = decltype(KC)::value;
+                        constexpr uint32_t off_q = (kk >> 2) * Cfg::kQAtomBytes + (kk & 3) * 32;
+                        constexpr uint32_t off_k = (kk >> 2) * Cfg::kKVAtomBytes + (kk & 3) * 32;
+                        mma_ss_off<((T * Cfg::kQBytes + off_q) >> 4), ((KSL * Cfg::kKVBytes + off_k) >> 4)>(
+                            kTmem + s_col, dq, dk, Cfg::kIdescS, kk ? 1u : 0u);
+                    });
                     mma_commit(&bar_sfull[T]);
                     TRACE(12 + T, j);
                 };
                 if (pend0) {
                     pv(std::integral_constant<int, 0>{}, acc0, pphase0);
                     pend0 = false;
+                }
+                if (j < L) {
+                    mbar_wait(&bar_full[KSL], ((2 * j) / kSlots) & 1);
+                    TRACE(16, j);
+                    tc_fence_after();
                 }
                 if (tf0) {
                     qk(std::integral_constant<int, 0>{});
@@ -271,16 +290,19 @@ __global__ void __launch_bounds__(kThreads, 1)
                     pv(std::integral_constant<int, 1>{}, acc1, pphase1);
                     pend1 = false;
                 }
+                if (j > 0) mma_commit(&bar_empty[VSL]);  // V_{j-1} free once its PVs finish
                 if (tf1) {
                     qk(std::integral_constant<int, 1>{});
                     pend1 = true;
                 }
-                if (j > 0) mma_commit(&bar_vempty[VSP]);
-                if (j < L) mma_commit(&bar_kempty[KS]);
+                if (j < L) mma_commit(&bar_empty[KSL]);
             };
-            for (uint32_t j = 0; j <= L; j += 2) {
+            for (uint32_t j = 0; j <= L; j += kSlots) {
                 step(j, std::integral_constant<int, 0>{});
                 if (j + 1 <= L) step(j + 1, std::integral_constant<int, 1>{});
+                if (j + 2 <= L) step(j + 2, std::integral_constant<int, 2>{});
+                if (j + 3 <= L) step(j + 3, std::integral_constant<int, 3>{});
+                if (j + 4 <= L) step(j + 4, std::integral_constant<int, 4>{});
             }
             mma_commit(&bar_ofull[0]);
             mma_commit(&bar_ofull[1]);
@@ -302,8 +324,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         const float sl2 = p.scale_log2;
         float m = -INFINITY, l = 0.f;
         uint32_t sphase = 0;
+#ifdef RADIAL_LOAD_ONLY
+        for (uint32_t j = 0; j < 0; ++j) {
+#else
+        uint32_t e_next = L > 0 ? entry(0) : 0u;
         for (uint32_t j = 0; j < L; ++j) {
-            const uint32_t e = entry(j);
+#endif
+            const uint32_t e = e_next;  // entry(j), loaded one iteration ahead
+            if (j + 1 < L) e_next = entry(j + 1);
             const uint32_t mask = e >> 28;
             if (((mask >> (t * Cfg::GT)) & ((1u << Cfg::GT) - 1)) == 0) continue;
             const uint32_t J = e & 0x0FFFFFFFu;
@@ -313,14 +341,31 @@ __global__ void __launch_bounds__(kThreads, 1)
             sphase ^= 1;
             tc_fence_after();
             float s[BK];
+            // first half, wait, then the second half's load overlaps the first half's max
 #pragma unroll
-            for (int c = 0; c < BK; c += 32) {
+            for (int c = 0; c < BK / 2; c += 32) {
                 uint32_t u[32];
                 tmem_ld32(s_addr + c, u);
 #pragma unroll
                 for (int x = 0; x < 32; ++x) s[c + x] = __uint_as_float(u[x]);
             }
             tmem_wait_ld();
+            float mh[8];
+#pragma unroll
+            for (int x = 0; x < 8; ++x) mh[x] = s[x];
+#pragma unroll
+            for (int c = BK / 2; c < BK; c += 32) {
+                uint32_t u[32];
+                tmem_ld32(s_addr + c, u);
+#pragma unroll
+                for (int x = 0; x < 32; ++x) s[c + x] = __uint_as_float(u[x]);
+            }
+#pragma unroll
+            for (int c = 8; c < BK / 2; c += 8)
+#pragma unroll
+                for (int x = 0; x < 8; ++x) mh[x] = fmaxf(mh[x], s[c + x]);
+            tmem_wait_ld();
+            if (warp == 4 && lane == 0) TRACE(14, j);
             const bool active = (mask >> my_bit) & 1;
             const uint64_t kv0 = static_cast<uint64_t>(J) * BK;
             const int valid = (kv0 + BK <= p.n) ? BK : static_cast<int>(p.n - kv0);
@@ -369,15 +414,25 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             // tree reduction: 8 independent chains instead of one 128-long chain
             float mm[8];
+            if (full) {
 #pragma unroll
-            for (int x = 0; x < 8; ++x) mm[x] = s[x];
+                for (int x = 0; x < 8; ++x) mm[x] = mh[x];
+            } else {
 #pragma unroll
-            for (int c = 8; c < BK; c += 8)
+                for (int x = 0; x < 8; ++x) mm[x] = s[x];
+#pragma unroll
+                for (int c = 8; c < BK / 2; c += 8)
+#pragma unroll
+                    for (int x = 0; x < 8; ++x) mm[x] = fmaxf(mm[x], s[c + x]);
+            }
+#pragma unroll
+            for (int c = BK / 2; c < BK; c += 8)
 #pragma unroll
                 for (int x = 0; x < 8; ++x) mm[x] = fmaxf(mm[x], s[c + x]);
             const float mx = fmaxf(fmaxf(fmaxf(mm[0], mm[1]), fmaxf(mm[2], mm[3])),
                                    fmaxf(fmaxf(mm[4], mm[5]), fmaxf(mm[6], mm[7])));
             const float m_cand = mx * sl2;
+            if (warp == 4 && lane == 0) TRACE(15, j);
             const bool need = active && (m == -INFINITY || m_cand > m + kRescaleThreshold);
             const bool rescale = need && m != -INFINITY;
             if (__any_sync(0xffffffffu, rescale)) {
@@ -411,8 +466,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                     if (((c >> 1) & 3) < NP) {
                         pr = ex2_poly2(x);  // FA4-style FMA-pipe exp2 for a share of columns
                     } else {
+#ifdef RADIAL_FAKE_EXP  // timing experiment only: no MUFU work (wrong results)
+                        pr = x;
+#else
                         pr.x = ex2(x.x);
                         pr.y = ex2(x.y);
+#endif
                     }
                     if ((c >> 1) & 1)
                         r2b = __fadd2_rn(r2b, pr);

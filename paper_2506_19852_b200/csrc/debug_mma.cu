@@ -196,3 +196,71 @@ extern "C" int radial_cuda_debug_mma_rate(int mode, int iters, int ctas, unsigne
         default: return RADIAL_ERR_INVALID;
     }
 }
+
+// ---------------------------------------------------------------------------
+// Elementwise pipe-rate microbenchmark (diagnostic hook): 148 CTAs x `warps`
+// warps, each thread runs 8 independent chains of one instruction kind and
+// reports SM clocks for `iters` x 8 instructions per thread.
+// op: 0 ex2.approx.ftz.f32, 1 ex2.approx.f16x2, 2 ex2.approx.ftz.bf16x2,
+//     3 cvt.rn.f16x2.f32, 4 cvt.rn.bf16x2.f32, 5 fma.rn.f32x2 (FFMA2),
+//     6 cvt f16x2 -> 2 x f32 (HADD2.F32), 7 max3 f32
+// ---------------------------------------------------------------------------
+namespace {
+template <int OP>
+__global__ void pipe_rate_kernel(int iters, unsigned long long* out, float seed) {
+    uint32_t r[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) r[i] = __float_as_uint(seed + 0.01f * (threadIdx.x + i));
+    __syncthreads();
+    const unsigned long long t0 = clock64();
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            if constexpr (OP == 0) {
+                asm volatile("ex2.approx.ftz.f32 %0, %0;" : "+r"(r[i]));
+            } else if constexpr (OP == 1) {
+                asm volatile("ex2.approx.f16x2 %0, %0;" : "+r"(r[i]));
+            } else if constexpr (OP == 2) {
+                asm volatile("ex2.approx.ftz.bf16x2 %0, %0;" : "+r"(r[i]));
+            } else if constexpr (OP == 3) {
+                asm volatile("cvt.rn.f16x2.f32 %0, %0, %0;" : "+r"(r[i]));
+            } else if constexpr (OP == 4) {
+                asm volatile("cvt.rn.bf16x2.f32 %0, %0, %0;" : "+r"(r[i]));
+            } else if constexpr (OP == 5) {
+                asm volatile("{.reg .b64 t; mov.b64 t, {%0, %0}; fma.rn.f32x2 t, t, t, t; mov.b64 {%0, _}, t;}" : "+r"(r[i]));
+            } else if constexpr (OP == 6) {
+                asm volatile("{.reg .f32 a, b; .reg .b16 l, h; mov.b32 {l, h}, %0; cvt.f32.f16 a, l; cvt.f32.f16 b, h; add.f32 a, a, b; mov.b32 %0, a;}" : "+r"(r[i]));
+            } else {
+                asm volatile("max.f32 %0, %0, %1, %2;" : "+r"(r[i]) : "r"(r[(i + 1) & 7]), "r"(r[(i + 2) & 7]));
+            }
+        }
+    }
+    __syncthreads();
+    const unsigned long long t1 = clock64();
+    uint32_t acc = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) acc ^= r[i];
+    if (threadIdx.x == 0) out[blockIdx.x] = (t1 - t0) | (acc == 0x12345678u ? 1ull << 63 : 0ull);
+}
+template <int OP>
+int run_pipe(int iters, int warps, unsigned long long* out_dev) {
+    pipe_rate_kernel<OP><<<148, warps * 32>>>(iters, out_dev, 0.37f);
+    RADIAL_CUDA_TRY(cudaGetLastError());
+    RADIAL_CUDA_TRY(cudaDeviceSynchronize());
+    return RADIAL_OK;
+}
+}  // namespace
+
+extern "C" int radial_cuda_debug_pipe_rate(int op, int iters, int warps, unsigned long long* out_dev) {
+    switch (op) {
+        case 0: return run_pipe<0>(iters, warps, out_dev);
+        case 1: return run_pipe<1>(iters, warps, out_dev);
+        case 2: return run_pipe<2>(iters, warps, out_dev);
+        case 3: return run_pipe<3>(iters, warps, out_dev);
+        case 4: return run_pipe<4>(iters, warps, out_dev);
+        case 5: return run_pipe<5>(iters, warps, out_dev);
+        case 6: return run_pipe<6>(iters, warps, out_dev);
+        case 7: return run_pipe<7>(iters, warps, out_dev);
+        default: return RADIAL_ERR_INVALID;
+    }
+}

@@ -18,7 +18,7 @@ def main():
     g = torch.Generator(device="cuda").manual_seed(0)
     q, k, v = (torch.randn(H, n, d, device="cuda", generator=g).to(torch.bfloat16) for _ in range(3))
     lay = P.device_layout(P.GridShape(f, s), P.PatternSpec.radial(), B)
-    CT, ST, EV = 4, 64, 16
+    CT, ST, EV = 4, 64, 24
     buf = torch.zeros(CT * ST * EV, dtype=torch.int64, device="cuda")
     lib = ctypes.CDLL(P.library_path())
     for _ in range(3):
@@ -28,7 +28,7 @@ def main():
     torch.cuda.synchronize()
     t = buf.view(CT, ST, EV).cpu().numpy().astype(np.int64)
     names = ["A.wait", "A.S", "A.P0", "A.P1", "B.wait", "B.S", "B.P0", "B.P1",
-             "M.PA0", "M.PA1", "M.PB0", "M.PB1", "M.SA", "M.SB"]
+             "M.PA0", "M.PA1", "M.PB0", "M.PB1", "M.SA", "M.SB", "A.ld", "A.max", "M.kfull", "M.vfull", "L.K", "L.V"]
     for c in range(CT):
         base = t[c, 1, 1]
         print(f"CTA {c}: times relative to step-1 A.S (clk)")
@@ -45,6 +45,9 @@ def main():
         print(" P arrive->MMA sees A0", d(2, 8), " A1", d(3, 9), " B0", d(6, 10), " B1", d(7, 11))
         print(" A.P1 -> next A.S (PV_A + S_A + latency):", d(3, 1, 1), " B:", d(7, 5, 1))
         print(" A wait-start -> S seen (idle):", d(0, 1))
+        print(" MMA: SB issued -> kfull(j+1) seen", d(13, 16, 1), " -> vfull seen", d(13, 17, 1), " K(j) load issue - S_B(j-2) seen", d(5, 18, 2), " V load issue", d(5, 19, 2))
+        print(" K(j) issue -> MMA kfull(j) seen", d(18, 16), " V(j) issue -> vfull seen (step j+1)", d(19, 17, 1))
+        print(" A: S seen -> ld done", d(1, 14), " ld -> max", d(14, 15), " max -> P0", d(15, 2))
 
 
 if __name__ == "__main__":
