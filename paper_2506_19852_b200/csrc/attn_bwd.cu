@@ -101,6 +101,7 @@ struct BwdCfg {
     static constexpr int kTileBytes = kBlk * D * 2;    // one 128-row bf16 tile
     static constexpr uint32_t kIdS = idesc_bf16(128, kSub, 0, 0);  // 128 x 64 x 16, K-major both
     static constexpr uint32_t kIdAcc = idesc_bf16(128, D, 0, 1);   // 128 x D x 16, B MN-major
+    static constexpr uint32_t kIdAcc128 = idesc_bf16(128, kBlk, 0, 0);  // 128 x 128 x 16, K-major both
 };
 
 // Base descriptors: an MMA's descriptor = base + (byte offset >> 4); the 14-bit start
@@ -133,8 +134,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                               const BwdParams p) {
     using Cfg = BwdCfg<D>;
     extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                               ~static_cast<uintptr_t>(1023));
+    uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     constexpr int T = Cfg::kTileBytes;
     // [Q | dO | K0 V0 | K1 V1]
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 6 * T);
@@ -184,7 +184,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     tma_load_3d(kd + T + a * Cfg::kAtomBytes, &tm_v, &bar_full[st], a * 64, J * kBlk, head);
                 }
             }
-        } else if (warp == 1 && lane == 0) {
+        } else if (warp == 1) {  // whole warp, converged (elected issue)
             // ------------------------------------------------ MMA issuer
             mbar_wait(bar_res, 0);
             tc_fence_after();
@@ -205,7 +205,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 tc_fence_after();
                 static_for<kSub / 16>([&](auto KK) {
                     constexpr int kk = decltype(KK)::value;
-                    mma_ts_off<((STG * 2 * T) >> 4) + mnoff(b * kSub + kk * 16)>(
+                    mma_ts_w<((STG * 2 * T) >> 4) + mnoff(b * kSub + kk * 16)>(
                         kTmem + 256, kTmem + b * 64 + kk * 8, dkv_mn, Cfg::kIdAcc, (acc || kk) ? 1u : 0u);
                 });
                 acc = true;
@@ -222,22 +222,22 @@ __global__ void __launch_bounds__(kThreads, 1)
                     // shared memory (an SS MMA at N = 64 is shared-memory bound)
                     static_for<D / 16>([&](auto KK) {
                         constexpr int kk = decltype(KK)::value;
-                        mma_ts_off<((STG * 2 * T) >> 4) + koff(kk, b * kSub)>(
+                        mma_ts_w<((STG * 2 * T) >> 4) + koff(kk, b * kSub)>(
                             kTmem + b * 64, kTmem + kColQ + kk * 8, dkv_k, Cfg::kIdS, kk ? 1u : 0u);
                     });
                     static_for<D / 16>([&](auto KK) {
                         constexpr int kk = decltype(KK)::value;
-                        mma_ts_off<((STG * 2 * T + T) >> 4) + koff(kk, b * kSub)>(
+                        mma_ts_w<((STG * 2 * T + T) >> 4) + koff(kk, b * kSub)>(
                             kTmem + 128 + b * 64, kTmem + kColDO + kk * 8, dkv_k, Cfg::kIdS, kk ? 1u : 0u);
                     });
-                    mma_commit(&bar_s[b]);
+                    mma_commit_w(&bar_s[b]);
                     BTRACE(1 + b, j);
                 };
                 sub(std::integral_constant<int, 0>{});
                 if (j > 0) {  // previous block's second sub-step, then free its K/V stage
                     dq_j = j - 1;
                     dq_mma(std::integral_constant<int, 1>{}, std::integral_constant<int, STG ^ 1>{});
-                    mma_commit(&bar_empty[STG ^ 1]);
+                    mma_commit_w(&bar_empty[STG ^ 1]);
                 }
                 sub(std::integral_constant<int, 1>{});
                 dq_j = j;
@@ -253,7 +253,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 else
                     dq_mma(std::integral_constant<int, 1>{}, std::integral_constant<int, 0>{});
             }
-            mma_commit(bar_acc);
+            mma_commit_w(bar_acc);
         }
     } else {
         regs_inc<200>();
@@ -359,8 +359,15 @@ __global__ void __launch_bounds__(kThreads, 1)
 }
 
 // ========================================================================== dK/dV
-// TMEM: S^T0 [0,64) S^T1 [64,128) dP^T0 [128,192) dP^T1 [192,256) dV [256,256+D) dK [256+D, 256+2D)
-// P^T (bf16) overwrites S^T_b columns [b*64, b*64+32); dS^T overwrites dP^T_b [128+b*64, +32).
+// CTA per (head, KV block J) over its CSC column; K_J, V_J resident in shared memory,
+// Q_I / dO_I streamed through two-stage rings.  Every MMA is 128 x 128 x 16 (N = 64
+// MMAs run at ~53 instead of 32 clk on B200, scripts/mma_rate.py).
+// TMEM: S^T [0,128) dP^T [128,256) dV [256,384) dK [384,512).
+// Warpgroup g owns query columns [64g, 64g+64): it writes P^T (bf16) over S^T columns
+// [64g, 64g+32) and dS^T over dP^T columns [128+64g, +32) -- inside its own range, so it
+// never overwrites values the other warpgroup has still to read.
+// MMA issue order per query block i:  S^T(i), dK(i-1), dP^T(i), dV(i), so the tensor core
+// computes dK(i-1) and dP^T(i) while the warpgroups turn S^T(i) into P^T(i).
 template <int D>
 __global__ void __launch_bounds__(kThreads, 1)
     radial_attn_bwd_dkdv_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_do,
@@ -368,19 +375,22 @@ __global__ void __launch_bounds__(kThreads, 1)
                                 const BwdParams p) {
     using Cfg = BwdCfg<D>;
     extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                               ~static_cast<uintptr_t>(1023));
+    uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     constexpr int T = Cfg::kTileBytes;
-    // [K | V | Q0 dO0 | Q1 dO1 | lse2/D stage0 (1 KB) | stage1 (1 KB)]
+    // [K | V | Q0 dO0 | Q1 dO1 | lse2/D stage0 (1 KB) | stage1 (1 KB) | barriers]
     float* vec = reinterpret_cast<float*>(smem + 6 * T);
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 6 * T + 2048);
-    uint64_t* bar_res = bars;
-    uint64_t* bar_full = bars + 1;
-    uint64_t* bar_empty = bars + 3;
-    uint64_t* bar_s = bars + 5;
-    uint64_t* bar_p = bars + 7;
-    uint64_t* bar_acc = bars + 9;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 10);
+    uint64_t* bar_res = bars;          // K, V landed
+    uint64_t* bar_qfull = bars + 1;    // [2] Q_i (+ lse2/D) landed
+    uint64_t* bar_qempty = bars + 3;   // [2] Q_i free (dK(i) done)
+    uint64_t* bar_dofull = bars + 5;   // [2]
+    uint64_t* bar_doempty = bars + 7;  // [2] dO_i free (dV(i) done)
+    uint64_t* bar_s = bars + 9;        // S^T(i) computed
+    uint64_t* bar_dp = bars + 10;      // dP^T(i) computed
+    uint64_t* bar_p = bars + 11;       // [2] P^T(i) query halves in TMEM (8 warp arrivals each)
+    uint64_t* bar_ds = bars + 13;      // dS^T(i) in TMEM (8 warp arrivals)
+    uint64_t* bar_acc = bars + 14;     // dV, dK final
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 15);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t head = blockIdx.x / p.R;
@@ -391,11 +401,16 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (warp == 0 && lane == 0) {
         mbar_init(bar_res, 1);
         for (int i = 0; i < 2; ++i) {
-            mbar_init(&bar_full[i], 1);
-            mbar_init(&bar_empty[i], 1);
-            mbar_init(&bar_s[i], 1);
-            mbar_init(&bar_p[i], 4);
+            mbar_init(&bar_qfull[i], 1);
+            mbar_init(&bar_qempty[i], 1);
+            mbar_init(&bar_dofull[i], 1);
+            mbar_init(&bar_doempty[i], 1);
         }
+        mbar_init(bar_s, 1);
+        mbar_init(bar_dp, 1);
+        mbar_init(&bar_p[0], 8);
+        mbar_init(&bar_p[1], 8);
+        mbar_init(bar_ds, 8);
         mbar_init(bar_acc, 1);
         fence_barrier_init();
     }
@@ -404,128 +419,176 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncthreads();
     tc_fence_after();
     if (*tmem_slot != 0) __trap();
+    constexpr uint32_t kColS = 0, kColDP = 128, kColDV = 256, kColDK = 384;
 
     if (warp < 4) {
         regs_dec<104>();
         if (warp == 0 && lane == 0) {
+            // ------------------------------------------------ producer
             mbar_arrive_expect_tx(bar_res, 2 * T);
             for (int a = 0; a < Cfg::kAtoms; ++a) {
                 tma_load_3d(smem + a * Cfg::kAtomBytes, &tm_k, bar_res, a * 64, J * kBlk, head);
                 tma_load_3d(smem + T + a * Cfg::kAtomBytes, &tm_v, bar_res, a * 64, J * kBlk, head);
             }
-            for (uint32_t j = 0; j < L; ++j) {
-                const int st = j & 1;
-                const uint32_t Iq = __ldg(p.idx + e0 + j);
-                mbar_wait(&bar_empty[st], ((j >> 1) & 1) ^ 1);
-                mbar_arrive_expect_tx(&bar_full[st], 2 * T + 2 * kBlk * 4);
+            for (uint32_t i = 0; i < L; ++i) {
+                const int st = i & 1;
+                const uint32_t Iq = __ldg(p.idx + e0 + i);
+                mbar_wait(&bar_qempty[st], ((i >> 1) & 1) ^ 1);
+                mbar_arrive_expect_tx(&bar_qfull[st], T + 2 * kBlk * 4);
                 uint8_t* qd = smem + (2 + 2 * st) * T;
-                for (int a = 0; a < Cfg::kAtoms; ++a) {
-                    tma_load_3d(qd + a * Cfg::kAtomBytes, &tm_q, &bar_full[st], a * 64, Iq * kBlk, head);
-                    tma_load_3d(qd + T + a * Cfg::kAtomBytes, &tm_do, &bar_full[st], a * 64, Iq * kBlk, head);
-                }
+                for (int a = 0; a < Cfg::kAtoms; ++a)
+                    tma_load_3d(qd + a * Cfg::kAtomBytes, &tm_q, &bar_qfull[st], a * 64, Iq * kBlk, head);
                 const uint64_t off = static_cast<uint64_t>(head) * p.rpad + static_cast<uint64_t>(Iq) * kBlk;
-                bulk_load(vec + st * 256, p.lse2 + off, kBlk * 4, &bar_full[st]);
-                bulk_load(vec + st * 256 + 128, p.dvec + off, kBlk * 4, &bar_full[st]);
+                bulk_load(vec + st * 256, p.lse2 + off, kBlk * 4, &bar_qfull[st]);
+                bulk_load(vec + st * 256 + 128, p.dvec + off, kBlk * 4, &bar_qfull[st]);
+                mbar_wait(&bar_doempty[st], ((i >> 1) & 1) ^ 1);
+                mbar_arrive_expect_tx(&bar_dofull[st], T);
+                for (int a = 0; a < Cfg::kAtoms; ++a)
+                    tma_load_3d(qd + T + a * Cfg::kAtomBytes, &tm_do, &bar_dofull[st], a * 64, Iq * kBlk, head);
             }
-        } else if (warp == 1 && lane == 0) {
+        } else if (warp == 1) {  // whole warp, converged (elected issue)
+            // ------------------------------------------------ MMA issuer
             mbar_wait(bar_res, 0);
             tc_fence_after();
-            const uint32_t k_s = smem_u32(smem), v_s = smem_u32(smem + T);
-            const uint32_t qd0 = smem_u32(smem + 2 * T);
-            uint32_t pph[2] = {0, 0};
-            bool acc = false;
-            // dV += P^T_b dO_sub ; dK += dS^T_b Q_sub   (K = 64 streamed rows)
-            auto acc_mma = [&](auto BC, uint32_t q_tile) {
-                constexpr int b = decltype(BC)::value;
-                mbar_wait(&bar_p[b], pph[b]);
-                pph[b] ^= 1;
-                tc_fence_after();
-                const uint32_t do_tile = q_tile + T;
-#pragma unroll
-                for (int kk = 0; kk < kSub / 16; ++kk)
-                    mma_ts(kTmem + 256, kTmem + b * 64 + kk * 8, mndesc(do_tile, b * kSub + kk * 16), Cfg::kIdAcc,
-                           (acc || kk) ? 1u : 0u);
-#pragma unroll
-                for (int kk = 0; kk < kSub / 16; ++kk)
-                    mma_ts(kTmem + 256 + D, kTmem + 128 + b * 64 + kk * 8, mndesc(q_tile, b * kSub + kk * 16),
-                           Cfg::kIdAcc, (acc || kk) ? 1u : 0u);
-                acc = true;
+            const uint64_t dkm = kbase(smem_u32(smem));        // K-major view of every tile
+            const uint64_t dmn = mnbase(smem_u32(smem));       // MN-major view
+            constexpr uint32_t kK = 0, kV = T, kQ0 = 2 * T;    // tile byte offsets
+            // dK += dS^T(i) Q_i  (A = dS^T from TMEM, B = Q_i MN-major, K = 128 queries)
+            auto dk_mma = [&](auto SC, bool first) {
+                constexpr int st = decltype(SC)::value;
+                static_for<kBlk / 16>([&](auto KK) {
+                    constexpr int kk = decltype(KK)::value;
+                    constexpr uint32_t a_col = kColDP + (kk >> 2) * 64 + (kk & 3) * 8;
+                    mma_ts_w<((kQ0 + st * 2 * T) >> 4) + mnoff(kk * 16)>(kTmem + kColDK, kTmem + a_col, dmn,
+                                                                          Cfg::kIdAcc, (!first || kk) ? 1u : 0u);
+                });
             };
-            for (uint32_t j = 0; j < L; ++j) {
-                const int st = j & 1;
-                const uint32_t q_t = qd0 + st * 2 * T, do_t = q_t + T;
-                const uint32_t q_prev = qd0 + (st ^ 1) * 2 * T;
-                mbar_wait(&bar_full[st], (j >> 1) & 1);
+            auto block = [&](uint32_t i, auto SC) {
+                constexpr int st = decltype(SC)::value;  // == i % 2
+                const uint32_t ph = (i >> 1) & 1;
+                // S^T(i) = K Q_i^T  (M = 128 keys, N = 128 queries, K = d)
+                mbar_wait(&bar_qfull[st], ph);
                 tc_fence_after();
-                auto sub = [&](auto BC) {
-                    constexpr int b = decltype(BC)::value;
-                    // S^T_b = K Q_sub^T ; dP^T_b = V dO_sub^T   (128 keys x 64 queries, K = d)
-#pragma unroll
-                    for (int kk = 0; kk < D / 16; ++kk)
-                        mma_ss(kTmem + b * 64, kdesc(k_s, kk, 0), kdesc(q_t, kk, b * kSub), Cfg::kIdS, kk ? 1u : 0u);
-#pragma unroll
-                    for (int kk = 0; kk < D / 16; ++kk)
-                        mma_ss(kTmem + 128 + b * 64, kdesc(v_s, kk, 0), kdesc(do_t, kk, b * kSub), Cfg::kIdS,
-                               kk ? 1u : 0u);
-                    mma_commit(&bar_s[b]);
-                };
-                sub(std::integral_constant<int, 0>{});
-                if (j > 0) {
-                    acc_mma(std::integral_constant<int, 1>{}, q_prev);
-                    mma_commit(&bar_empty[st ^ 1]);
+                static_for<D / 16>([&](auto KK) {
+                    constexpr int kk = decltype(KK)::value;
+                    mma_ss_w<koff(kk, 0) + (kK >> 4), koff(kk, 0) + ((kQ0 + st * 2 * T) >> 4)>(
+                        kTmem + kColS, dkm, dkm, Cfg::kIdAcc128, kk ? 1u : 0u);
+                });
+                mma_commit_w(bar_s);
+                BTRACE(0, i);
+                if (i > 0) {
+                    mbar_wait(bar_ds, (i - 1) & 1);
+                    tc_fence_after();
+                    dk_mma(std::integral_constant<int, st ^ 1>{}, i == 1);
+                    mma_commit_w(&bar_qempty[st ^ 1]);
+                    BTRACE(1, i);
                 }
-                sub(std::integral_constant<int, 1>{});
-                acc_mma(std::integral_constant<int, 0>{}, q_t);
+                // dP^T(i) = V dO_i^T
+                mbar_wait(&bar_dofull[st], ph);
+                tc_fence_after();
+                static_for<D / 16>([&](auto KK) {
+                    constexpr int kk = decltype(KK)::value;
+                    mma_ss_w<koff(kk, 0) + (kV >> 4), koff(kk, 0) + ((kQ0 + st * 2 * T + T) >> 4)>(
+                        kTmem + kColDP, dkm, dkm, Cfg::kIdAcc128, kk ? 1u : 0u);
+                });
+                mma_commit_w(bar_dp);
+                BTRACE(2, i);
+                // dV += P^T(i) dO_i, in two query halves (h = 0: queries 0-31 and 64-95,
+                // h = 1: 32-63 and 96-127) so the first starts while the second's
+                // exponentials are still being computed
+                static_for<2>([&](auto HC) {
+                    constexpr int h = decltype(HC)::value;
+                    mbar_wait(&bar_p[h], i & 1);
+                    if (h == 0) BTRACE(3, i);
+                    tc_fence_after();
+                    static_for<4>([&](auto KK) {
+                        constexpr int kk = (decltype(KK)::value >> 1) * 4 + h * 2 + (decltype(KK)::value & 1);
+                        constexpr uint32_t a_col = kColS + (kk >> 2) * 64 + (kk & 3) * 8;
+                        mma_ts_w<((kQ0 + st * 2 * T + T) >> 4) + mnoff(kk * 16)>(
+                            kTmem + kColDV, kTmem + a_col, dmn, Cfg::kIdAcc, (i > 0 || kk) ? 1u : 0u);
+                    });
+                });
+                mma_commit_w(&bar_doempty[st]);
+                BTRACE(4, i);
+            };
+            for (uint32_t i = 0; i < L; i += 2) {
+                block(i, std::integral_constant<int, 0>{});
+                if (i + 1 < L) block(i + 1, std::integral_constant<int, 1>{});
             }
-            if (L > 0) acc_mma(std::integral_constant<int, 1>{}, qd0 + ((L - 1) & 1) * 2 * T);
-            mma_commit(bar_acc);
+            if (L > 0) {
+                mbar_wait(bar_ds, (L - 1) & 1);
+                tc_fence_after();
+                if ((L - 1) & 1)
+                    dk_mma(std::integral_constant<int, 1>{}, L == 1);
+                else
+                    dk_mma(std::integral_constant<int, 0>{}, L == 1);
+            }
+            mma_commit_w(bar_acc);
         }
     } else {
         regs_inc<200>();
-        const int wg = (warp - 4) >> 2;
+        const int wg = (warp - 4) >> 2;  // query columns [64 wg, 64 wg + 64)
         const int r = ((warp & 3) << 5) + lane;  // key row of the tile
         const uint32_t la = static_cast<uint32_t>((warp & 3) * 32) << 16;
         const uint64_t krow = static_cast<uint64_t>(J) * kBlk + r;
         const float sl2 = p.scale_log2;
-        for (uint32_t j = 0; j < L; ++j) {
-            const int st = j & 1;
-            mbar_wait(&bar_s[wg], j & 1);
+        for (uint32_t i = 0; i < L; ++i) {
+            const int st = i & 1;
+            mbar_wait(bar_s, i & 1);
+            if (warp == 4 && lane == 0) BTRACE(5, i);
             tc_fence_after();
-            uint32_t sv[64], dp[64];
-            tmem_ld32(kTmem + la + wg * 64, *reinterpret_cast<uint32_t(*)[32]>(sv));
-            tmem_ld32(kTmem + la + wg * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(sv + 32));
-            tmem_ld32(kTmem + la + 128 + wg * 64, *reinterpret_cast<uint32_t(*)[32]>(dp));
-            tmem_ld32(kTmem + la + 128 + wg * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(dp + 32));
+            uint32_t sv[64];
+            tmem_ld32(kTmem + la + kColS + wg * 64, *reinterpret_cast<uint32_t(*)[32]>(sv));
+            tmem_ld32(kTmem + la + kColS + wg * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(sv + 32));
             tmem_wait_ld();
-            // lse2 / D of the 64 query columns (already landed with this stage's Q/dO)
-            const float4* lv = reinterpret_cast<const float4*>(vec + st * 256 + wg * kSub);
-            const float4* dvv = reinterpret_cast<const float4*>(vec + st * 256 + 128 + wg * kSub);
-            uint32_t pp[32], pd[32];
+            const float4* lv = reinterpret_cast<const float4*>(vec + st * 256 + wg * 64);
+            float pv[64];
 #pragma unroll
-            for (int c4 = 0; c4 < kSub / 4; ++c4) {
-                const float4 l4 = lv[c4], d4 = dvv[c4];
-                const float ls[4] = {l4.x, l4.y, l4.z, l4.w};
-                const float ds_[4] = {d4.x, d4.y, d4.z, d4.w};
-                float pv[4], dv[4];
+            for (int h = 0; h < 2; ++h) {
+                uint32_t pp[16];
 #pragma unroll
-                for (int x = 0; x < 4; ++x) {
-                    const int c = c4 * 4 + x;
-                    pv[x] = ex2(fmaf(__uint_as_float(sv[c]), sl2, -ls[x]));
-                    dv[x] = pv[x] * (__uint_as_float(dp[c]) - ds_[x]);
+                for (int c4 = 8 * h; c4 < 8 * h + 8; ++c4) {
+                    const float4 l4 = lv[c4];
+                    pv[4 * c4 + 0] = ex2(fmaf(__uint_as_float(sv[4 * c4 + 0]), sl2, -l4.x));
+                    pv[4 * c4 + 1] = ex2(fmaf(__uint_as_float(sv[4 * c4 + 1]), sl2, -l4.y));
+                    pv[4 * c4 + 2] = ex2(fmaf(__uint_as_float(sv[4 * c4 + 2]), sl2, -l4.z));
+                    pv[4 * c4 + 3] = ex2(fmaf(__uint_as_float(sv[4 * c4 + 3]), sl2, -l4.w));
+                    pp[2 * (c4 - 8 * h)] = pack_bf16(pv[4 * c4], pv[4 * c4 + 1]);
+                    pp[2 * (c4 - 8 * h) + 1] = pack_bf16(pv[4 * c4 + 2], pv[4 * c4 + 3]);
                 }
-                pp[c4 * 2] = pack_bf16(pv[0], pv[1]);
-                pp[c4 * 2 + 1] = pack_bf16(pv[2], pv[3]);
-                pd[c4 * 2] = pack_bf16(dv[0], dv[1]);
-                pd[c4 * 2 + 1] = pack_bf16(dv[2], dv[3]);
+                tmem_st16(kTmem + la + kColS + wg * 64 + 16 * h, pp);
+                tmem_wait_st();
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&bar_p[h]);
             }
-            tmem_st16(kTmem + la + wg * 64, pp);
-            tmem_st16(kTmem + la + wg * 64 + 16, pp + 16);
-            tmem_st16(kTmem + la + 128 + wg * 64, pd);
-            tmem_st16(kTmem + la + 128 + wg * 64 + 16, pd + 16);
+            if ((warp == 4 || warp == 8) && lane == 0) BTRACE(warp == 4 ? 7 : 10, i);
+            mbar_wait(bar_dp, i & 1);
+            if (warp == 4 && lane == 0) BTRACE(8, i);
+            tc_fence_after();
+            uint32_t dp[64];
+            tmem_ld32(kTmem + la + kColDP + wg * 64, *reinterpret_cast<uint32_t(*)[32]>(dp));
+            tmem_ld32(kTmem + la + kColDP + wg * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(dp + 32));
+            tmem_wait_ld();
+            const float4* dvv = reinterpret_cast<const float4*>(vec + st * 256 + 128 + wg * 64);
+            uint32_t pd[32];
+#pragma unroll
+            for (int c4 = 0; c4 < 16; ++c4) {
+                const float4 d4 = dvv[c4];
+                const float a0 = pv[4 * c4 + 0] * (__uint_as_float(dp[4 * c4 + 0]) - d4.x);
+                const float a1 = pv[4 * c4 + 1] * (__uint_as_float(dp[4 * c4 + 1]) - d4.y);
+                const float a2 = pv[4 * c4 + 2] * (__uint_as_float(dp[4 * c4 + 2]) - d4.z);
+                const float a3 = pv[4 * c4 + 3] * (__uint_as_float(dp[4 * c4 + 3]) - d4.w);
+                pd[2 * c4] = pack_bf16(a0, a1);
+                pd[2 * c4 + 1] = pack_bf16(a2, a3);
+            }
+            tmem_st16(kTmem + la + kColDP + wg * 64, pd);
+            tmem_st16(kTmem + la + kColDP + wg * 64 + 16, pd + 16);
             tmem_wait_st();
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(&bar_p[wg]);
+            if (lane == 0) mbar_arrive(bar_ds);
+            if ((warp == 4 || warp == 8) && lane == 0) BTRACE(warp == 4 ? 9 : 11, i);
         }
         // ---------------------------------------------------- epilogue: wg0 -> dV, wg1 -> dK * scale
         mbar_wait(bar_acc, 0);
@@ -535,13 +598,13 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int c = 0; c < D; c += 32) {
             uint32_t u[32];
-            tmem_ld32(kTmem + la + 256 + wg * D + c, u);
+            tmem_ld32(kTmem + la + (wg ? kColDK : kColDV) + c, u);
             tmem_wait_ld();
             if (krow < p.n) {
                 uint32_t w[16];
 #pragma unroll
                 for (int x = 0; x < 16; ++x)
-                    w[x] = pack_bf16(__uint_as_float(u[2 * x]) * mul, __uint_as_float(u[2 * x + 1]) * mul);
+                    w[x] = L ? pack_bf16(__uint_as_float(u[2 * x]) * mul, __uint_as_float(u[2 * x + 1]) * mul) : 0u;
                 uint4* dst = reinterpret_cast<uint4*>(out + c);
 #pragma unroll
                 for (int x = 0; x < 4; ++x) dst[x] = make_uint4(w[4 * x], w[4 * x + 1], w[4 * x + 2], w[4 * x + 3]);
@@ -608,7 +671,7 @@ int launch_bwd_t(const void* q, const void* k, const void* v, const void* o, con
     }
     {
         const int smem = 6 * T + 2048 + 128 + 1024;
-        auto kern = radial_attn_bwd_dkdv_kernel<D>;
+        auto kern = radial_attn_bwd_dkdv_kernel<D>;  // 6 tiles: K, V, 2 x (Q, dO)
         RADIAL_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         p.ptr = L->col_ptr;
         p.idx = L->row_idx;

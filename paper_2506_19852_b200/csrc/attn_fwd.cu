@@ -48,6 +48,19 @@ constexpr int kTraceCtas = 4, kTraceSteps = 64, kTraceEv = 24;
 
 namespace {
 
+// MMA issue from lane 0 of warp 1 (measured 2-3% faster here than the warp-converged
+// elect.sync issue the backward kernels use; build with -DRADIAL_FWD_WARP_MMA to compare)
+#ifndef RADIAL_FWD_WARP_MMA
+#define RADIAL_FWD_LANE0 1
+#define FWD_MMA_SS mma_ss_off
+#define FWD_MMA_TS mma_ts_off
+#define FWD_COMMIT mma_commit
+#else
+#define FWD_MMA_SS mma_ss_w
+#define FWD_MMA_TS mma_ts_w
+#define FWD_COMMIT mma_commit_w
+#endif
+
 constexpr int kThreads = 384;
 constexpr uint32_t kTmem = 0;   // TMEM base address (checked against tcgen05.alloc)
 constexpr int kBQ = 128;        // query rows per tile
@@ -203,7 +216,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         // the ring depth so stage indices are constants.  That keeps the operands in
         // uniform registers; a per-MMA register->uniform move would otherwise double
         // the issue cost of each 128x128x16 MMA (measured: 114 vs 64 clk).
+#ifdef RADIAL_FWD_LANE0
         if (lane == 0) {
+#else
+        {  // whole warp, converged: elect.sync inside the MMA / commit wrappers
+#endif
             mbar_wait(bar_q, 0);
             tc_fence_after();
             // base descriptors; an MMA's descriptor = base + (byte offset >> 4) (the 14-bit
@@ -249,7 +266,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         tc_fence_after();
                         static_for<BK / 32>([&](auto KI) {
                             constexpr int kk = h * (BK / 32) + decltype(KI)::value;
-                            mma_ts_off<((VSL * Cfg::kKVBytes + kk * 16 * 128) >> 4)>(
+                            FWD_MMA_TS<((VSL * Cfg::kKVBytes + kk * 16 * 128) >> 4)>(
                                 kTmem + o_col, kTmem + p_col + kk * 8, dv, Cfg::kIdescO, (acc | kk) ? 1u : 0u);
                         });
                     });
@@ -267,10 +284,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                         constexpr int kk = decltype(KC)::value;
                         constexpr uint32_t off_q = (kk >> 2) * Cfg::kQAtomBytes + (kk & 3) * 32;
                         constexpr uint32_t off_k = (kk >> 2) * Cfg::kKVAtomBytes + (kk & 3) * 32;
-                        mma_ss_off<((T * Cfg::kQBytes + off_q) >> 4), ((KSL * Cfg::kKVBytes + off_k) >> 4)>(
+                        FWD_MMA_SS<((T * Cfg::kQBytes + off_q) >> 4), ((KSL * Cfg::kKVBytes + off_k) >> 4)>(
                             kTmem + s_col, dq, dk, Cfg::kIdescS, kk ? 1u : 0u);
                     });
-                    mma_commit(&bar_sfull[T]);
+                    FWD_COMMIT(&bar_sfull[T]);
                     TRACE(12 + T, j);
                 };
                 if (pend0) {
@@ -290,12 +307,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                     pv(std::integral_constant<int, 1>{}, acc1, pphase1);
                     pend1 = false;
                 }
-                if (j > 0) mma_commit(&bar_empty[VSL]);  // V_{j-1} free once its PVs finish
+                if (j > 0) FWD_COMMIT(&bar_empty[VSL]);  // V_{j-1} free once its PVs finish
                 if (tf1) {
                     qk(std::integral_constant<int, 1>{});
                     pend1 = true;
                 }
-                if (j < L) mma_commit(&bar_empty[KSL]);
+                if (j < L) FWD_COMMIT(&bar_empty[KSL]);
             };
             for (uint32_t j = 0; j <= L; j += kSlots) {
                 step(j, std::integral_constant<int, 0>{});
@@ -304,8 +321,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (j + 3 <= L) step(j + 3, std::integral_constant<int, 3>{});
                 if (j + 4 <= L) step(j + 4, std::integral_constant<int, 4>{});
             }
-            mma_commit(&bar_ofull[0]);
-            mma_commit(&bar_ofull[1]);
+            FWD_COMMIT(&bar_ofull[0]);
+            FWD_COMMIT(&bar_ofull[1]);
         }
     }
     } else {

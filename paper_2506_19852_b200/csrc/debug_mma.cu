@@ -184,7 +184,7 @@ int run_rate(int iters, int ctas, unsigned long long* out_dev) {
     return RADIAL_OK;
 }
 
-// mode: bit0 TS, bit1 N=256, bit2 two accumulators
+// mode: bit0 TS, bit1 N=256, bit2 two accumulators; 6 / 7 = SS / TS N=64
 extern "C" int radial_cuda_debug_mma_rate(int mode, int iters, int ctas, unsigned long long* out_dev) {
     switch (mode & 7) {
         case 0: return run_rate<false, 128, 1>(iters, ctas, out_dev);
@@ -193,6 +193,8 @@ extern "C" int radial_cuda_debug_mma_rate(int mode, int iters, int ctas, unsigne
         case 3: return run_rate<true, 256, 1>(iters, ctas, out_dev);
         case 4: return run_rate<false, 128, 2>(iters, ctas, out_dev);
         case 5: return run_rate<true, 128, 2>(iters, ctas, out_dev);
+        case 6: return run_rate<false, 64, 1>(iters, ctas, out_dev);
+        case 7: return run_rate<true, 64, 1>(iters, ctas, out_dev);
         default: return RADIAL_ERR_INVALID;
     }
 }
@@ -263,4 +265,87 @@ extern "C" int radial_cuda_debug_pipe_rate(int op, int iters, int warps, unsigne
         case 7: return run_pipe<7>(iters, warps, out_dev);
         default: return RADIAL_ERR_INVALID;
     }
+}
+
+// ---------------------------------------------------------------------------
+// Interference microbenchmark (diagnostic hook): one thread issues back-to-back
+// 128x128x16 SS MMAs into TMEM columns [0,128) while 8 other warps either idle
+// (mode 0), stream tcgen05.ld of columns [256,384) (mode 1), tcgen05.ld + st
+// (mode 2), or ld.shared from an unrelated smem region (mode 3).  Reports SM
+// clocks per MMA.
+// ---------------------------------------------------------------------------
+namespace {
+__global__ void __launch_bounds__(384, 1) mma_interf_kernel(int mode, int iters, unsigned long long* out) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + 160 * 1024);
+    uint32_t* slot = reinterpret_cast<uint32_t*>(bar + 2);
+    volatile uint32_t* stop = reinterpret_cast<volatile uint32_t*>(bar + 3);
+    const int warp = threadIdx.x >> 5;
+    for (int i = threadIdx.x; i < 160 * 1024 / 16; i += blockDim.x)
+        reinterpret_cast<uint4*>(smem)[i] = make_uint4(0x3c003c00u, 0, 0x3c003c00u, 0);
+    if (threadIdx.x == 0) {
+        mbar_init(bar, 1);
+        *stop = 0;
+        fence_barrier_init();
+    }
+    if (warp == 1) tmem_alloc(slot, 512);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    if (*slot != 0) __trap();
+    if (threadIdx.x == 0) {
+        const uint64_t da = sdesc_sw128(smem_u32(smem), 16, 1024), db = sdesc_sw128(smem_u32(smem + 32768), 16, 1024);
+        constexpr uint32_t idesc = idesc_bf16(128, 128, 0, 0);
+        const unsigned long long t0 = clock64();
+        for (int it = 0; it < iters; ++it) {
+            static_for<8>([&](auto KK) {
+                constexpr int kk = decltype(KK)::value;
+                constexpr uint32_t off = static_cast<uint32_t>(((kk >> 2) * 16384 + (kk & 3) * 32) >> 4);
+                mma_ss_off<off, off>(0u, da, db, idesc, 1u);
+            });
+        }
+        mma_commit(bar);
+        mbar_wait(bar, 0);
+        const unsigned long long t1 = clock64();
+        out[blockIdx.x] = t1 - t0;
+        *stop = 1;
+    } else if (warp >= 4 && mode > 0) {
+        const uint32_t la = static_cast<uint32_t>((warp & 3) * 32) << 16;
+        uint32_t acc = 0;
+        while (*stop == 0) {
+            if (mode == 3) {
+                const uint4* src = reinterpret_cast<const uint4*>(smem + 65536 + (threadIdx.x & 127) * 16);
+#pragma unroll
+                for (int x = 0; x < 16; ++x) acc += src[x * 128].x;
+            } else {
+                uint32_t u[32];
+                tmem_ld32(la + 256 + ((warp >> 2) & 1) * 64, u);
+                tmem_wait_ld();
+                acc += u[3];
+                if (mode == 2) {
+                    tmem_st16(la + 384 + ((warp >> 2) & 1) * 64, u);
+                    tmem_wait_st();
+                }
+            }
+        }
+        if (acc == 0x12345u) out[gridDim.x] = acc;
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        tmem_dealloc(*slot, 512);
+    }
+}
+}  // namespace
+
+extern "C" int radial_cuda_debug_mma_interference(int mode, int iters, unsigned long long* out_dev) {
+    const int smem = 160 * 1024 + 64 + 1024;
+    RADIAL_CUDA_TRY(cudaFuncSetAttribute(mma_interf_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    mma_interf_kernel<<<148, 384, smem>>>(mode, iters, out_dev);
+    RADIAL_CUDA_TRY(cudaGetLastError());
+    RADIAL_CUDA_TRY(cudaDeviceSynchronize());
+    return RADIAL_OK;
 }

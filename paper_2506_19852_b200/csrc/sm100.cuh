@@ -164,6 +164,45 @@ __device__ __forceinline__ void mma_ts_off(uint32_t d_tmem, uint32_t a_tmem, uin
         "r"(a_tmem), "l"(b_base), "r"(idesc), "r"(accumulate), "n"(OB)
         : "memory");
 }
+// Warp-converged variants: the whole (converged) warp calls these and elect.sync picks
+// the issuing lane inside the asm.  ptxas can then keep every operand in uniform
+// registers and emits back-to-back UTCHMMA; a call from a single divergent lane is
+// wrapped in an ELECT / R2UR / BRA.U.ANY loop of ~15 instructions per MMA, which
+// limits the issue rate below the tensor core's 64 clk per 128x128x16 MMA.
+template <uint32_t OA, uint32_t OB>
+__device__ __forceinline__ void mma_ss_w(uint32_t d_tmem, uint64_t a_base, uint64_t b_base,
+                                         uint32_t idesc, uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p, e;\n\t.reg .b64 da, db;\n\t"
+        "add.s64 da, %1, %5;\n\t"
+        "add.s64 db, %2, %6;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], da, db, %3, p;\n\t}" ::"r"(d_tmem),
+        "l"(a_base), "l"(b_base), "r"(idesc), "r"(accumulate), "n"(OA), "n"(OB)
+        : "memory");
+}
+template <uint32_t OB>
+__device__ __forceinline__ void mma_ts_w(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_base,
+                                         uint32_t idesc, uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p, e;\n\t.reg .b64 db;\n\t"
+        "add.s64 db, %2, %5;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], db, %3, p;\n\t}" ::"r"(d_tmem),
+        "r"(a_tmem), "l"(b_base), "r"(idesc), "r"(accumulate), "n"(OB)
+        : "memory");
+}
+// Warp-converged tcgen05.commit (one elected lane arrives).
+__device__ __forceinline__ void mma_commit_w(uint64_t* bar) {
+    asm volatile(
+        "{\n\t.reg .pred e;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(
+            smem_u32(bar))
+        : "memory");
+}
 // Compile-time loop: f(std::integral_constant<int, I>) for I in [0, N).
 template <int N, class F, int... Is>
 __device__ __forceinline__ void static_for_impl(F&& f, std::integer_sequence<int, Is...>) {

@@ -16,7 +16,7 @@ def main():
     lib = ctypes.CDLL(P.library_path())
     out = torch.zeros(148, dtype=torch.int64, device="cuda")
     iters = 4096
-    for warps in (8, 16):
+    for warps in (4, 8, 16):
         for op in range(8):
             assert lib.radial_cuda_debug_pipe_rate(op, iters, warps, ctypes.c_void_p(out.data_ptr())) == 0
             cyc = (out & ((1 << 62) - 1)).double().mean().item()
