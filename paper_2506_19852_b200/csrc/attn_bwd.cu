@@ -18,6 +18,7 @@
 // sub-step s+1 while warpgroup (s mod 2) does the elementwise work of s.
 // Block size 128 only (the layouts of the BASELINE backward configs).
 #include <cmath>
+#include <cstdlib>
 #include <type_traits>
 
 #include "radial_internal.h"
@@ -125,8 +126,14 @@ __device__ __forceinline__ uint64_t mndesc(uint32_t tile, int row0) {
 }
 
 // ============================================================================ dQ
-// TMEM: S0 [0,64) S1 [64,128) dP0 [128,192) dP1 [192,256) dQ [256,256+D) Q [384,448) dO [448,512)
-constexpr uint32_t kColQ = 384, kColDO = 448;
+// CTA per (head, query block I) over its CSR row.  Q is resident in TMEM (A operand of
+// S = Q K^T), dO in shared memory (A operand of dP = dO V^T); K_j / V_j stream through
+// 3- / 2-stage rings.  Every MMA is 128 x 128 x 16.
+// TMEM: S [0,128) dP [128,256) dQ [256,256+D) dS [256+D, 320+D) Q [320+D, 320+D+D/2).
+// Warpgroup g owns key columns [64g, 64g+64).  The warpgroups release S and dP as soon
+// as they have loaded them, so the tensor core computes S(j+1) and dP(j+1) while they
+// turn block j into dS(j); dS has its own columns, freed when dQ(j) has consumed it.
+// MMA issue order per block j:  S(j), dP(j), dQ(j-1).
 template <int D>
 __global__ void __launch_bounds__(kThreads, 1)
     radial_attn_bwd_dq_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_do,
@@ -136,15 +143,24 @@ __global__ void __launch_bounds__(kThreads, 1)
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     constexpr int T = Cfg::kTileBytes;
-    // [Q | dO | K0 V0 | K1 V1]
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 6 * T);
-    uint64_t* bar_res = bars;          // Q, dO landed
-    uint64_t* bar_full = bars + 1;     // [2] K/V stage landed
-    uint64_t* bar_empty = bars + 3;    // [2] K/V stage free
-    uint64_t* bar_s = bars + 5;        // [2] S/dP sub-buffer computed
-    uint64_t* bar_ds = bars + 7;       // [2] dS sub-buffer written
-    uint64_t* bar_acc = bars + 9;      // dQ final
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 10);
+    constexpr int kKS = 3, kVS = 2;  // ring depths
+    // [dO | K0 K1 K2 | V0 V1 | barriers]
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (1 + kKS + kVS) * T);
+    uint64_t* bar_q = bars;            // Q rows stored into TMEM (8 warp arrivals)
+    uint64_t* bar_do = bars + 1;       // dO landed
+    uint64_t* bar_kfull = bars + 2;    // [3]
+    uint64_t* bar_kempty = bars + 5;   // [3] K_j free (dQ(j) done)
+    uint64_t* bar_vfull = bars + 8;    // [2]
+    uint64_t* bar_vempty = bars + 10;  // [2] V_j free (dP(j) done)
+    uint64_t* bar_s = bars + 12;       // S(j) computed
+    uint64_t* bar_dp = bars + 13;      // dP(j) computed
+    uint64_t* bar_sfree = bars + 14;   // S(j) loaded by the warpgroups (8)
+    uint64_t* bar_dpfree = bars + 15;  // dP(j) loaded (8)
+    uint64_t* bar_ds = bars + 16;      // dS(j) in TMEM (8)
+    uint64_t* bar_dsfree = bars + 17;  // dQ(j) done: dS columns free
+    uint64_t* bar_acc = bars + 18;     // dQ final
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 19);
+    constexpr uint32_t kColS = 0, kColDP = 128, kColDQ = 256, kColDS = 256 + D, kColQ = 320 + D;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t head = blockIdx.x / p.R;
@@ -153,13 +169,22 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t L = static_cast<uint32_t>(p.ptr[I + 1] - e0);
 
     if (warp == 0 && lane == 0) {
-        mbar_init(bar_res, 8);  // Q / dO rows stored into TMEM by the 8 elementwise warps
-        for (int i = 0; i < 2; ++i) {
-            mbar_init(&bar_full[i], 1);
-            mbar_init(&bar_empty[i], 1);
-            mbar_init(&bar_s[i], 1);
-            mbar_init(&bar_ds[i], 4);
+        mbar_init(bar_q, 8);
+        mbar_init(bar_do, 1);
+        for (int i = 0; i < kKS; ++i) {
+            mbar_init(&bar_kfull[i], 1);
+            mbar_init(&bar_kempty[i], 1);
         }
+        for (int i = 0; i < kVS; ++i) {
+            mbar_init(&bar_vfull[i], 1);
+            mbar_init(&bar_vempty[i], 1);
+        }
+        mbar_init(bar_s, 1);
+        mbar_init(bar_dp, 1);
+        mbar_init(bar_sfree, 8);
+        mbar_init(bar_dpfree, 8);
+        mbar_init(bar_ds, 8);
+        mbar_init(bar_dsfree, 1);
         mbar_init(bar_acc, 1);
         fence_barrier_init();
     }
@@ -173,103 +198,109 @@ __global__ void __launch_bounds__(kThreads, 1)
         regs_dec<104>();
         if (warp == 0 && lane == 0) {
             // ------------------------------------------------ producer
+            mbar_arrive_expect_tx(bar_do, T);
+            for (int a = 0; a < Cfg::kAtoms; ++a)
+                tma_load_3d(smem + a * Cfg::kAtomBytes, &tm_do, bar_do, a * 64, I * kBlk, head);
             for (uint32_t j = 0; j < L; ++j) {
-                const int st = j & 1;
                 const int32_t J = static_cast<int32_t>(__ldg(p.idx + e0 + j));
-                mbar_wait(&bar_empty[st], ((j >> 1) & 1) ^ 1);
-                mbar_arrive_expect_tx(&bar_full[st], 2 * T);
-                uint8_t* kd = smem + (2 + 2 * st) * T;
-                for (int a = 0; a < Cfg::kAtoms; ++a) {
-                    tma_load_3d(kd + a * Cfg::kAtomBytes, &tm_k, &bar_full[st], a * 64, J * kBlk, head);
-                    tma_load_3d(kd + T + a * Cfg::kAtomBytes, &tm_v, &bar_full[st], a * 64, J * kBlk, head);
-                }
+                const int ks = j % kKS, vs = j % kVS;
+                mbar_wait(&bar_kempty[ks], ((j / kKS) & 1) ^ 1);
+                mbar_arrive_expect_tx(&bar_kfull[ks], T);
+                for (int a = 0; a < Cfg::kAtoms; ++a)
+                    tma_load_3d(smem + (1 + ks) * T + a * Cfg::kAtomBytes, &tm_k, &bar_kfull[ks], a * 64, J * kBlk, head);
+                mbar_wait(&bar_vempty[vs], ((j / kVS) & 1) ^ 1);
+                mbar_arrive_expect_tx(&bar_vfull[vs], T);
+                for (int a = 0; a < Cfg::kAtoms; ++a)
+                    tma_load_3d(smem + (1 + kKS + vs) * T + a * Cfg::kAtomBytes, &tm_v, &bar_vfull[vs], a * 64,
+                                J * kBlk, head);
             }
         } else if (warp == 1) {  // whole warp, converged (elected issue)
             // ------------------------------------------------ MMA issuer
-            mbar_wait(bar_res, 0);
+            mbar_wait(bar_q, 0);
+            mbar_wait(bar_do, 0);
             tc_fence_after();
-            const uint64_t dkv_k = kbase(smem_u32(smem + 2 * T));  // K/V stages, K-major view
-            const uint64_t dkv_mn = mnbase(smem_u32(smem + 2 * T));  // K/V stages, MN-major view
-            uint32_t dsph0 = 0, dsph1 = 0;
-            bool acc = false;
-            uint32_t dq_j = 0;  // block index of the dS being consumed (trace only)
-            (void)dq_j;
-            // dQ += dS(sub-buffer b) . K(rows of that sub-step), K in stage STG
-            auto dq_mma = [&](auto BC, auto SC) {
-                constexpr int b = decltype(BC)::value;
-                constexpr int STG = decltype(SC)::value;
-                uint32_t& ph = b ? dsph1 : dsph0;
-                mbar_wait(&bar_ds[b], ph);
-                BTRACE(3 + b, dq_j);
-                ph ^= 1;
-                tc_fence_after();
-                static_for<kSub / 16>([&](auto KK) {
+            const uint64_t dkm = kbase(smem_u32(smem));  // K-major view of every tile
+            const uint64_t dmn = mnbase(smem_u32(smem));  // MN-major view
+            // dQ += dS(j) K_j  (A = dS from TMEM, B = K_j MN-major, K = 128 keys)
+            auto dq_mma = [&](auto KSC, bool first) {
+                constexpr int ks = decltype(KSC)::value;
+                static_for<kBlk / 16>([&](auto KK) {
                     constexpr int kk = decltype(KK)::value;
-                    mma_ts_w<((STG * 2 * T) >> 4) + mnoff(b * kSub + kk * 16)>(
-                        kTmem + 256, kTmem + b * 64 + kk * 8, dkv_mn, Cfg::kIdAcc, (acc || kk) ? 1u : 0u);
+                    mma_ts_w<(((1 + ks) * T) >> 4) + mnoff(kk * 16)>(kTmem + kColDQ, kTmem + kColDS + kk * 8, dmn,
+                                                                    Cfg::kIdAcc, (!first || kk) ? 1u : 0u);
                 });
-                acc = true;
             };
-            auto block = [&](uint32_t j, auto SC) {
-                constexpr int STG = decltype(SC)::value;  // == j % 2
-                mbar_wait(&bar_full[STG], (j >> 1) & 1);
-                BTRACE(0, j);
+            // step j: ring slots are compile-time constants (the loop is unrolled by 6 =
+            // lcm of the ring depths)
+            auto block = [&](uint32_t j, auto PC) {
+                constexpr int P6 = decltype(PC)::value;  // == j % 6
+                constexpr int ks = P6 % kKS, vs = P6 % kVS, ksp = (P6 + kKS - 1) % kKS;
+                // S(j) = Q K_j^T  (TS: Q from TMEM)
+                mbar_wait(&bar_kfull[ks], (j / kKS) & 1);
+                if (j > 0) mbar_wait(bar_sfree, (j - 1) & 1);
                 tc_fence_after();
-                auto sub = [&](auto BC) {
-                    constexpr int b = decltype(BC)::value;
-                    // S_b = Q K_sub^T ; dP_b = dO V_sub^T   (128 x 64, K = d): TS MMAs with
-                    // Q / dO read from TMEM, so only the 64-row K / V sub-tile streams from
-                    // shared memory (an SS MMA at N = 64 is shared-memory bound)
-                    static_for<D / 16>([&](auto KK) {
-                        constexpr int kk = decltype(KK)::value;
-                        mma_ts_w<((STG * 2 * T) >> 4) + koff(kk, b * kSub)>(
-                            kTmem + b * 64, kTmem + kColQ + kk * 8, dkv_k, Cfg::kIdS, kk ? 1u : 0u);
-                    });
-                    static_for<D / 16>([&](auto KK) {
-                        constexpr int kk = decltype(KK)::value;
-                        mma_ts_w<((STG * 2 * T + T) >> 4) + koff(kk, b * kSub)>(
-                            kTmem + 128 + b * 64, kTmem + kColDO + kk * 8, dkv_k, Cfg::kIdS, kk ? 1u : 0u);
-                    });
-                    mma_commit_w(&bar_s[b]);
-                    BTRACE(1 + b, j);
-                };
-                sub(std::integral_constant<int, 0>{});
-                if (j > 0) {  // previous block's second sub-step, then free its K/V stage
-                    dq_j = j - 1;
-                    dq_mma(std::integral_constant<int, 1>{}, std::integral_constant<int, STG ^ 1>{});
-                    mma_commit_w(&bar_empty[STG ^ 1]);
+                static_for<D / 16>([&](auto KK) {
+                    constexpr int kk = decltype(KK)::value;
+                    mma_ts_w<koff(kk, 0) + (((1 + ks) * T) >> 4)>(kTmem + kColS, kTmem + kColQ + kk * 8, dkm,
+                                                                   Cfg::kIdAcc128, kk ? 1u : 0u);
+                });
+                mma_commit_w(bar_s);
+                BTRACE(1, j);
+                // dP(j) = dO V_j^T  (SS)
+                mbar_wait(&bar_vfull[vs], (j / kVS) & 1);
+                if (j > 0) mbar_wait(bar_dpfree, (j - 1) & 1);
+                tc_fence_after();
+                static_for<D / 16>([&](auto KK) {
+                    constexpr int kk = decltype(KK)::value;
+                    mma_ss_w<koff(kk, 0), koff(kk, 0) + (((1 + kKS + vs) * T) >> 4)>(kTmem + kColDP, dkm, dkm,
+                                                                                   Cfg::kIdAcc128, kk ? 1u : 0u);
+                });
+                mma_commit_w(bar_dp);
+                mma_commit_w(&bar_vempty[vs]);
+                BTRACE(2, j);
+                // dQ += dS(j-1) K_{j-1}
+                if (j > 0) {
+                    mbar_wait(bar_ds, (j - 1) & 1);
+                    BTRACE(3, j);
+                    tc_fence_after();
+                    dq_mma(std::integral_constant<int, ksp>{}, j == 1);
+                    mma_commit_w(&bar_kempty[ksp]);
+                    mma_commit_w(bar_dsfree);
                 }
-                sub(std::integral_constant<int, 1>{});
-                dq_j = j;
-                dq_mma(std::integral_constant<int, 0>{}, std::integral_constant<int, STG>{});
             };
-            for (uint32_t j = 0; j < L; j += 2) {
+            for (uint32_t j = 0; j < L; j += 6) {
                 block(j, std::integral_constant<int, 0>{});
                 if (j + 1 < L) block(j + 1, std::integral_constant<int, 1>{});
+                if (j + 2 < L) block(j + 2, std::integral_constant<int, 2>{});
+                if (j + 3 < L) block(j + 3, std::integral_constant<int, 3>{});
+                if (j + 4 < L) block(j + 4, std::integral_constant<int, 4>{});
+                if (j + 5 < L) block(j + 5, std::integral_constant<int, 5>{});
             }
             if (L > 0) {
-                if ((L - 1) & 1)
-                    dq_mma(std::integral_constant<int, 1>{}, std::integral_constant<int, 1>{});
-                else
-                    dq_mma(std::integral_constant<int, 1>{}, std::integral_constant<int, 0>{});
+                mbar_wait(bar_ds, (L - 1) & 1);
+                tc_fence_after();
+                switch ((L - 1) % kKS) {
+                    case 0: dq_mma(std::integral_constant<int, 0>{}, L == 1); break;
+                    case 1: dq_mma(std::integral_constant<int, 1>{}, L == 1); break;
+                    default: dq_mma(std::integral_constant<int, 2>{}, L == 1); break;
+                }
             }
             mma_commit_w(bar_acc);
         }
     } else {
         regs_inc<200>();
         // ---------------------------------------------------- elementwise
-        const int wg = (warp - 4) >> 2;  // sub-buffer this warpgroup owns
+        const int wg = (warp - 4) >> 2;  // key columns [64 wg, 64 wg + 64)
         const int r = ((warp & 3) << 5) + lane;
         const uint32_t la = static_cast<uint32_t>((warp & 3) * 32) << 16;
         const uint64_t row = static_cast<uint64_t>(I) * kBlk + r;
         const uint64_t prow = static_cast<uint64_t>(head) * p.rpad + row;
         {
-            // resident A operands: warpgroup 0 stores this row of Q, warpgroup 1 of dO, as
-            // packed bf16 pairs in TMEM (lane = row, column c = elements 2c, 2c+1)
-            const __nv_bfloat16* src = (wg ? p.dout : p.q) + (static_cast<uint64_t>(head) * p.n + row) * D;
-            const uint32_t col = wg ? kColDO : kColQ;
+            // resident A operand: this row of Q as packed bf16 pairs in TMEM (lane = row,
+            // column c = elements 2c, 2c+1); warpgroup g stores elements [D/2 g, D/2 (g+1))
+            const __nv_bfloat16* src = p.q + (static_cast<uint64_t>(head) * p.n + row) * D + wg * (D / 2);
 #pragma unroll
-            for (int c = 0; c < D / 2; c += 16) {
+            for (int c = 0; c < D / 4; c += 16) {
                 uint32_t w[16];
                 if (row < p.n) {
                     const uint4* g = reinterpret_cast<const uint4*>(src + 2 * c);
@@ -285,50 +316,59 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                     for (int x = 0; x < 16; ++x) w[x] = 0u;
                 }
-                tmem_st16(kTmem + la + col + c, w);
+                tmem_st16(kTmem + la + kColQ + wg * (D / 4) + c, w);
             }
             tmem_wait_st();
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(bar_res);
+            if (lane == 0) mbar_arrive(bar_q);
         }
         const float lse2 = p.lse2[prow];
         const float dval = p.dvec[prow];
         const float sl2 = p.scale_log2;
         for (uint32_t j = 0; j < L; ++j) {
             const uint32_t J = __ldg(p.idx + e0 + j);
-            if ((warp & 3) == 0 && lane == 0) BTRACE(5 + 2 * wg, j);
-            mbar_wait(&bar_s[wg], j & 1);
-            if ((warp & 3) == 0 && lane == 0) BTRACE(5 + 2 * wg, j);
+            mbar_wait(bar_s, j & 1);
+            if (warp == 4 && lane == 0) BTRACE(5, j);
             tc_fence_after();
-            uint32_t sv[64], dp[64];
-            tmem_ld32(kTmem + la + wg * 64, *reinterpret_cast<uint32_t(*)[32]>(sv));
-            tmem_ld32(kTmem + la + wg * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(sv + 32));
-            tmem_ld32(kTmem + la + 128 + wg * 64, *reinterpret_cast<uint32_t(*)[32]>(dp));
-            tmem_ld32(kTmem + la + 128 + wg * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(dp + 32));
+            uint32_t sv[64];
+            tmem_ld32(kTmem + la + kColS + wg * 64, *reinterpret_cast<uint32_t(*)[32]>(sv));
+            tmem_ld32(kTmem + la + kColS + wg * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(sv + 32));
             tmem_wait_ld();
-            const uint64_t key0 = static_cast<uint64_t>(J) * kBlk + wg * kSub;
-            const int valid = key0 + kSub <= p.n ? kSub : (key0 < p.n ? static_cast<int>(p.n - key0) : 0);
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(bar_sfree);
+            const uint64_t key0 = static_cast<uint64_t>(J) * kBlk + wg * 64;
+            const int valid = key0 + 64 <= p.n ? 64 : (key0 < p.n ? static_cast<int>(p.n - key0) : 0);
+            float pv[64];
+#pragma unroll
+            for (int c = 0; c < 64; ++c) pv[c] = ex2(fmaf(__uint_as_float(sv[c]), sl2, -lse2));
+            if (valid < 64) {
+#pragma unroll
+                for (int c = 0; c < 64; ++c) pv[c] = c < valid ? pv[c] : 0.f;
+            }
+            mbar_wait(bar_dp, j & 1);
+            tc_fence_after();
+            uint32_t dp[64];
+            tmem_ld32(kTmem + la + kColDP + wg * 64, *reinterpret_cast<uint32_t(*)[32]>(dp));
+            tmem_ld32(kTmem + la + kColDP + wg * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(dp + 32));
+            tmem_wait_ld();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(bar_dpfree);
             uint32_t pk[32];
 #pragma unroll
-            for (int c = 0; c < kSub; c += 2) {
-                float p0 = ex2(fmaf(__uint_as_float(sv[c]), sl2, -lse2));
-                float p1 = ex2(fmaf(__uint_as_float(sv[c + 1]), sl2, -lse2));
-                if (valid < kSub) {
-                    p0 = c < valid ? p0 : 0.f;
-                    p1 = c + 1 < valid ? p1 : 0.f;
-                }
-                const float d0 = p0 * (__uint_as_float(dp[c]) - dval);
-                const float d1 = p1 * (__uint_as_float(dp[c + 1]) - dval);
-                pk[c / 2] = pack_bf16(d0, d1);
-            }
-            tmem_st16(kTmem + la + wg * 64, pk);
-            tmem_st16(kTmem + la + wg * 64 + 16, pk + 16);
+            for (int c = 0; c < 64; c += 2)
+                pk[c / 2] = pack_bf16(pv[c] * (__uint_as_float(dp[c]) - dval), pv[c + 1] * (__uint_as_float(dp[c + 1]) - dval));
+            if (j > 0) mbar_wait(bar_dsfree, (j - 1) & 1);
+            tc_fence_after();
+            tmem_st16(kTmem + la + kColDS + wg * 32, pk);
+            tmem_st16(kTmem + la + kColDS + wg * 32 + 16, pk + 16);
             tmem_wait_st();
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(&bar_ds[wg]);
-            if ((warp & 3) == 0 && lane == 0) BTRACE(6 + 2 * wg, j);
+            if (lane == 0) mbar_arrive(bar_ds);
+            if (warp == 4 && lane == 0) BTRACE(6, j);
         }
         // ---------------------------------------------------- epilogue: dQ * scale
         mbar_wait(bar_acc, 0);
@@ -337,13 +377,13 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int c = 0; c < kHalf; c += 32) {
             uint32_t u[32];
-            tmem_ld32(kTmem + la + 256 + wg * kHalf + c, u);
+            tmem_ld32(kTmem + la + kColDQ + wg * kHalf + c, u);
             tmem_wait_ld();
             if (row < p.n) {
                 uint32_t w[16];
 #pragma unroll
                 for (int x = 0; x < 16; ++x)
-                    w[x] = pack_bf16(__uint_as_float(u[2 * x]) * p.scale, __uint_as_float(u[2 * x + 1]) * p.scale);
+                    w[x] = L ? pack_bf16(__uint_as_float(u[2 * x]) * p.scale, __uint_as_float(u[2 * x + 1]) * p.scale) : 0u;
                 uint4* dst = reinterpret_cast<uint4*>(p.dq + (static_cast<uint64_t>(head) * p.n + row) * D + wg * kHalf + c);
 #pragma unroll
                 for (int x = 0; x < 4; ++x) dst[x] = make_uint4(w[4 * x], w[4 * x + 1], w[4 * x + 2], w[4 * x + 3]);
@@ -660,7 +700,7 @@ int launch_bwd_t(const void* q, const void* k, const void* v, const void* o, con
     if (items > 0x7fffffffull) return fail(RADIAL_ERR_INVALID, "attn_bwd: too many work items");
     const int T = BwdCfg<D>::kTileBytes;
     {
-        const int smem = 6 * T + 128 + 1024;
+        const int smem = 6 * T + 256 + 1024;  // dO, 3 K + 2 V stages, barriers
         auto kern = radial_attn_bwd_dq_kernel<D>;
         RADIAL_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         p.ptr = L->row_ptr;
@@ -669,6 +709,9 @@ int launch_bwd_t(const void* q, const void* k, const void* v, const void* o, con
         kern<<<static_cast<unsigned>(items), kThreads, smem, st>>>(tq, tdo, tk, tv, p);
         RADIAL_CUDA_TRY(cudaGetLastError());
     }
+#ifdef RADIAL_TRACE
+    if (getenv("RADIAL_BWD_DQ_ONLY")) return RADIAL_OK;  // trace builds: time the dQ kernel alone
+#endif
     {
         const int smem = 6 * T + 2048 + 128 + 1024;
         auto kern = radial_attn_bwd_dkdv_kernel<D>;  // 6 tiles: K, V, 2 x (Q, dO)
