@@ -341,8 +341,13 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint64_t key0 = static_cast<uint64_t>(J) * kBlk + wg * 64;
             const int valid = key0 + 64 <= p.n ? 64 : (key0 < p.n ? static_cast<int>(p.n - key0) : 0);
             float pv[64];
+            const float2 sl = make_float2(sl2, sl2), nl = make_float2(-lse2, -lse2);
 #pragma unroll
-            for (int c = 0; c < 64; ++c) pv[c] = ex2(fmaf(__uint_as_float(sv[c]), sl2, -lse2));
+            for (int c = 0; c < 64; c += 2) {
+                const float2 x = __ffma2_rn(make_float2(__uint_as_float(sv[c]), __uint_as_float(sv[c + 1])), sl, nl);
+                pv[c] = ex2(x.x);
+                pv[c + 1] = ex2(x.y);
+            }
             if (valid < 64) {
 #pragma unroll
                 for (int c = 0; c < 64; ++c) pv[c] = c < valid ? pv[c] : 0.f;
@@ -357,9 +362,13 @@ __global__ void __launch_bounds__(kThreads, 1)
             __syncwarp();
             if (lane == 0) mbar_arrive(bar_dpfree);
             uint32_t pk[32];
+            const float2 nd = make_float2(-dval, -dval);
 #pragma unroll
-            for (int c = 0; c < 64; c += 2)
-                pk[c / 2] = pack_bf16(pv[c] * (__uint_as_float(dp[c]) - dval), pv[c + 1] * (__uint_as_float(dp[c + 1]) - dval));
+            for (int c = 0; c < 64; c += 2) {
+                const float2 g = __fadd2_rn(make_float2(__uint_as_float(dp[c]), __uint_as_float(dp[c + 1])), nd);
+                const float2 ds = __fmul2_rn(make_float2(pv[c], pv[c + 1]), g);
+                pk[c / 2] = pack_bf16(ds.x, ds.y);
+            }
             if (j > 0) mbar_wait(bar_dsfree, (j - 1) & 1);
             tc_fence_after();
             tmem_st16(kTmem + la + kColDS + wg * 32, pk);
@@ -589,10 +598,15 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                 for (int c4 = 8 * h; c4 < 8 * h + 8; ++c4) {
                     const float4 l4 = lv[c4];
-                    pv[4 * c4 + 0] = ex2(fmaf(__uint_as_float(sv[4 * c4 + 0]), sl2, -l4.x));
-                    pv[4 * c4 + 1] = ex2(fmaf(__uint_as_float(sv[4 * c4 + 1]), sl2, -l4.y));
-                    pv[4 * c4 + 2] = ex2(fmaf(__uint_as_float(sv[4 * c4 + 2]), sl2, -l4.z));
-                    pv[4 * c4 + 3] = ex2(fmaf(__uint_as_float(sv[4 * c4 + 3]), sl2, -l4.w));
+                    const float2 sl = make_float2(sl2, sl2);
+                    const float2 xa = __ffma2_rn(make_float2(__uint_as_float(sv[4 * c4]), __uint_as_float(sv[4 * c4 + 1])),
+                                                 sl, make_float2(-l4.x, -l4.y));
+                    const float2 xb = __ffma2_rn(make_float2(__uint_as_float(sv[4 * c4 + 2]), __uint_as_float(sv[4 * c4 + 3])),
+                                                 sl, make_float2(-l4.z, -l4.w));
+                    pv[4 * c4 + 0] = ex2(xa.x);
+                    pv[4 * c4 + 1] = ex2(xa.y);
+                    pv[4 * c4 + 2] = ex2(xb.x);
+                    pv[4 * c4 + 3] = ex2(xb.y);
                     pp[2 * (c4 - 8 * h)] = pack_bf16(pv[4 * c4], pv[4 * c4 + 1]);
                     pp[2 * (c4 - 8 * h) + 1] = pack_bf16(pv[4 * c4 + 2], pv[4 * c4 + 3]);
                 }
@@ -615,12 +629,14 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int c4 = 0; c4 < 16; ++c4) {
                 const float4 d4 = dvv[c4];
-                const float a0 = pv[4 * c4 + 0] * (__uint_as_float(dp[4 * c4 + 0]) - d4.x);
-                const float a1 = pv[4 * c4 + 1] * (__uint_as_float(dp[4 * c4 + 1]) - d4.y);
-                const float a2 = pv[4 * c4 + 2] * (__uint_as_float(dp[4 * c4 + 2]) - d4.z);
-                const float a3 = pv[4 * c4 + 3] * (__uint_as_float(dp[4 * c4 + 3]) - d4.w);
-                pd[2 * c4] = pack_bf16(a0, a1);
-                pd[2 * c4 + 1] = pack_bf16(a2, a3);
+                const float2 ga = __fadd2_rn(make_float2(__uint_as_float(dp[4 * c4]), __uint_as_float(dp[4 * c4 + 1])),
+                                             make_float2(-d4.x, -d4.y));
+                const float2 gb = __fadd2_rn(make_float2(__uint_as_float(dp[4 * c4 + 2]), __uint_as_float(dp[4 * c4 + 3])),
+                                             make_float2(-d4.z, -d4.w));
+                const float2 a = __fmul2_rn(make_float2(pv[4 * c4], pv[4 * c4 + 1]), ga);
+                const float2 b = __fmul2_rn(make_float2(pv[4 * c4 + 2], pv[4 * c4 + 3]), gb);
+                pd[2 * c4] = pack_bf16(a.x, a.y);
+                pd[2 * c4 + 1] = pack_bf16(b.x, b.y);
             }
             tmem_st16(kTmem + la + kColDP + wg * 64, pd);
             tmem_st16(kTmem + la + kColDP + wg * 64 + 16, pd + 16);
