@@ -409,14 +409,15 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 // ========================================================================== dK/dV
 // CTA per (head, KV block J) over its CSC column; K_J, V_J resident in shared memory,
-// Q_I / dO_I streamed through two-stage rings.  Every MMA is 128 x 128 x 16 (N = 64
-// MMAs run at ~53 instead of 32 clk on B200, scripts/mma_rate.py).
+// Q_I through a 3-stage ring, dO_I (+ lse2 / D of its rows) through a 2-stage ring.
+// Every MMA is 128 x 128 x 16 (N = 64 MMAs run at ~53 instead of 32 clk on B200).
 // TMEM: S^T [0,128) dP^T [128,256) dV [256,384) dK [384,512).
-// Warpgroup g owns query columns [64g, 64g+64): it writes P^T (bf16) over S^T columns
-// [64g, 64g+32) and dS^T over dP^T columns [128+64g, +32) -- inside its own range, so it
-// never overwrites values the other warpgroup has still to read.
-// MMA issue order per query block i:  S^T(i), dK(i-1), dP^T(i), dV(i), so the tensor core
-// computes dK(i-1) and dP^T(i) while the warpgroups turn S^T(i) into P^T(i).
+// The warpgroups release S^T(i) as soon as they have loaded it, so S^T(i+1) is computed
+// while they work on block i.  Warpgroup g owns query columns [64g, 64g+64); once it has
+// loaded its dP^T(i) columns it writes P^T(i) (bf16) to [128+64g, +32) and dS^T(i) to
+// [128+64g+32, +32) -- inside its own range, never over values the other one still reads.
+// MMA issue order per query block i:  dP^T(i), S^T(i+1), dV(i), dK(i).  The warpgroups'
+// exponentials for block i run while the tensor core computes dK(i-1) and dP^T(i).
 template <int D>
 __global__ void __launch_bounds__(kThreads, 1)
     radial_attn_bwd_dkdv_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_do,
@@ -424,22 +425,28 @@ __global__ void __launch_bounds__(kThreads, 1)
                                 const BwdParams p) {
     using Cfg = BwdCfg<D>;
     extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+    // the dynamic window starts 1 KB-aligned on sm_100 (checked): no alignment slack, the
+    // 3 + 2 stage rings use 226 KB of the 227 KB
+    if (smem_u32(smem_raw) & 1023u) __trap();
+    uint8_t* smem = smem_raw;
     constexpr int T = Cfg::kTileBytes;
-    // [K | V | Q0 dO0 | Q1 dO1 | lse2/D stage0 (1 KB) | stage1 (1 KB) | barriers]
-    float* vec = reinterpret_cast<float*>(smem + 6 * T);
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 6 * T + 2048);
+    constexpr int kQS = 3, kDS = 2;
+    // [K | V | Q0 Q1 Q2 | dO0 dO1 | lse2/D for dO stage 0 (1 KB), stage 1 (1 KB) | barriers]
+    constexpr int kOffQ = 2 * T, kOffDO = kOffQ + kQS * T;
+    float* vec = reinterpret_cast<float*>(smem + kOffDO + kDS * T);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kOffDO + kDS * T + 2048);
     uint64_t* bar_res = bars;          // K, V landed
-    uint64_t* bar_qfull = bars + 1;    // [2] Q_i (+ lse2/D) landed
-    uint64_t* bar_qempty = bars + 3;   // [2] Q_i free (dK(i) done)
-    uint64_t* bar_dofull = bars + 5;   // [2]
-    uint64_t* bar_doempty = bars + 7;  // [2] dO_i free (dV(i) done)
-    uint64_t* bar_s = bars + 9;        // S^T(i) computed
-    uint64_t* bar_dp = bars + 10;      // dP^T(i) computed
-    uint64_t* bar_p = bars + 11;       // [2] P^T(i) query halves in TMEM (8 warp arrivals each)
-    uint64_t* bar_ds = bars + 13;      // dS^T(i) in TMEM (8 warp arrivals)
-    uint64_t* bar_acc = bars + 14;     // dV, dK final
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 15);
+    uint64_t* bar_qfull = bars + 1;    // [3] Q_i landed
+    uint64_t* bar_qempty = bars + 4;   // [3] Q_i free (dK(i) done)
+    uint64_t* bar_dofull = bars + 7;   // [2] dO_i + lse2/D landed
+    uint64_t* bar_doempty = bars + 9;  // [2] dO_i free (dV(i) done; the warpgroups are past block i)
+    uint64_t* bar_s = bars + 11;       // S^T(i) computed
+    uint64_t* bar_sfree = bars + 12;   // S^T(i) loaded by the warpgroups (8)
+    uint64_t* bar_dp = bars + 13;      // dP^T(i) computed
+    uint64_t* bar_p = bars + 14;       // [2] P^T(i) query halves in TMEM (8 each)
+    uint64_t* bar_ds = bars + 16;      // dS^T(i) in TMEM (8)
+    uint64_t* bar_acc = bars + 17;     // dV, dK final
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 18);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t head = blockIdx.x / p.R;
@@ -449,13 +456,16 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     if (warp == 0 && lane == 0) {
         mbar_init(bar_res, 1);
-        for (int i = 0; i < 2; ++i) {
+        for (int i = 0; i < kQS; ++i) {
             mbar_init(&bar_qfull[i], 1);
             mbar_init(&bar_qempty[i], 1);
+        }
+        for (int i = 0; i < kDS; ++i) {
             mbar_init(&bar_dofull[i], 1);
             mbar_init(&bar_doempty[i], 1);
         }
         mbar_init(bar_s, 1);
+        mbar_init(bar_sfree, 8);
         mbar_init(bar_dp, 1);
         mbar_init(&bar_p[0], 8);
         mbar_init(&bar_p[1], 8);
@@ -480,20 +490,21 @@ __global__ void __launch_bounds__(kThreads, 1)
                 tma_load_3d(smem + T + a * Cfg::kAtomBytes, &tm_v, bar_res, a * 64, J * kBlk, head);
             }
             for (uint32_t i = 0; i < L; ++i) {
-                const int st = i & 1;
+                const int qs = i % kQS, ds = i % kDS;
                 const uint32_t Iq = __ldg(p.idx + e0 + i);
-                mbar_wait(&bar_qempty[st], ((i >> 1) & 1) ^ 1);
-                mbar_arrive_expect_tx(&bar_qfull[st], T + 2 * kBlk * 4);
-                uint8_t* qd = smem + (2 + 2 * st) * T;
+                mbar_wait(&bar_qempty[qs], ((i / kQS) & 1) ^ 1);
+                mbar_arrive_expect_tx(&bar_qfull[qs], T);
                 for (int a = 0; a < Cfg::kAtoms; ++a)
-                    tma_load_3d(qd + a * Cfg::kAtomBytes, &tm_q, &bar_qfull[st], a * 64, Iq * kBlk, head);
+                    tma_load_3d(smem + kOffQ + qs * T + a * Cfg::kAtomBytes, &tm_q, &bar_qfull[qs], a * 64,
+                                Iq * kBlk, head);
+                mbar_wait(&bar_doempty[ds], ((i / kDS) & 1) ^ 1);
+                mbar_arrive_expect_tx(&bar_dofull[ds], T + 2 * kBlk * 4);
+                for (int a = 0; a < Cfg::kAtoms; ++a)
+                    tma_load_3d(smem + kOffDO + ds * T + a * Cfg::kAtomBytes, &tm_do, &bar_dofull[ds], a * 64,
+                                Iq * kBlk, head);
                 const uint64_t off = static_cast<uint64_t>(head) * p.rpad + static_cast<uint64_t>(Iq) * kBlk;
-                bulk_load(vec + st * 256, p.lse2 + off, kBlk * 4, &bar_qfull[st]);
-                bulk_load(vec + st * 256 + 128, p.dvec + off, kBlk * 4, &bar_qfull[st]);
-                mbar_wait(&bar_doempty[st], ((i >> 1) & 1) ^ 1);
-                mbar_arrive_expect_tx(&bar_dofull[st], T);
-                for (int a = 0; a < Cfg::kAtoms; ++a)
-                    tma_load_3d(qd + T + a * Cfg::kAtomBytes, &tm_do, &bar_dofull[st], a * 64, Iq * kBlk, head);
+                bulk_load(vec + ds * 256, p.lse2 + off, kBlk * 4, &bar_dofull[ds]);
+                bulk_load(vec + ds * 256 + 128, p.dvec + off, kBlk * 4, &bar_dofull[ds]);
             }
         } else if (warp == 1) {  // whole warp, converged (elected issue)
             // ------------------------------------------------ MMA issuer
@@ -501,50 +512,38 @@ __global__ void __launch_bounds__(kThreads, 1)
             tc_fence_after();
             const uint64_t dkm = kbase(smem_u32(smem));        // K-major view of every tile
             const uint64_t dmn = mnbase(smem_u32(smem));       // MN-major view
-            constexpr uint32_t kK = 0, kV = T, kQ0 = 2 * T;    // tile byte offsets
-            // dK += dS^T(i) Q_i  (A = dS^T from TMEM, B = Q_i MN-major, K = 128 queries)
-            auto dk_mma = [&](auto SC, bool first) {
-                constexpr int st = decltype(SC)::value;
-                static_for<kBlk / 16>([&](auto KK) {
-                    constexpr int kk = decltype(KK)::value;
-                    constexpr uint32_t a_col = kColDP + (kk >> 2) * 64 + (kk & 3) * 8;
-                    mma_ts_w<((kQ0 + st * 2 * T) >> 4) + mnoff(kk * 16)>(kTmem + kColDK, kTmem + a_col, dmn,
-                                                                          Cfg::kIdAcc, (!first || kk) ? 1u : 0u);
-                });
-            };
-            auto block = [&](uint32_t i, auto SC) {
-                constexpr int st = decltype(SC)::value;  // == i % 2
-                const uint32_t ph = (i >> 1) & 1;
-                // S^T(i) = K Q_i^T  (M = 128 keys, N = 128 queries, K = d)
-                mbar_wait(&bar_qfull[st], ph);
+            constexpr uint32_t kK = 0, kV = T;                 // tile byte offsets
+            // S^T(i) = K Q_i^T  (M = 128 keys, N = 128 queries, K = d)
+            auto s_mma = [&](uint32_t i, auto QC) {
+                constexpr int qs = decltype(QC)::value;
+                mbar_wait(&bar_qfull[qs], (i / kQS) & 1);
+                if (i > 0) mbar_wait(bar_sfree, (i - 1) & 1);
                 tc_fence_after();
                 static_for<D / 16>([&](auto KK) {
                     constexpr int kk = decltype(KK)::value;
-                    mma_ss_w<koff(kk, 0) + (kK >> 4), koff(kk, 0) + ((kQ0 + st * 2 * T) >> 4)>(
+                    mma_ss_w<koff(kk, 0) + (kK >> 4), koff(kk, 0) + ((kOffQ + qs * T) >> 4)>(
                         kTmem + kColS, dkm, dkm, Cfg::kIdAcc128, kk ? 1u : 0u);
                 });
                 mma_commit_w(bar_s);
                 BTRACE(0, i);
-                if (i > 0) {
-                    mbar_wait(bar_ds, (i - 1) & 1);
-                    tc_fence_after();
-                    dk_mma(std::integral_constant<int, st ^ 1>{}, i == 1);
-                    mma_commit_w(&bar_qempty[st ^ 1]);
-                    BTRACE(1, i);
-                }
+            };
+            // step i (P6 = i % 6 keeps every ring slot a compile-time constant)
+            auto block = [&](uint32_t i, auto PC) {
+                constexpr int P6 = decltype(PC)::value;
+                constexpr int qs = P6 % kQS, ds = P6 % kDS, qn = (P6 + 1) % kQS;
                 // dP^T(i) = V dO_i^T
-                mbar_wait(&bar_dofull[st], ph);
+                mbar_wait(&bar_dofull[ds], (i / kDS) & 1);
                 tc_fence_after();
                 static_for<D / 16>([&](auto KK) {
                     constexpr int kk = decltype(KK)::value;
-                    mma_ss_w<koff(kk, 0) + (kV >> 4), koff(kk, 0) + ((kQ0 + st * 2 * T + T) >> 4)>(
+                    mma_ss_w<koff(kk, 0) + (kV >> 4), koff(kk, 0) + ((kOffDO + ds * T) >> 4)>(
                         kTmem + kColDP, dkm, dkm, Cfg::kIdAcc128, kk ? 1u : 0u);
                 });
                 mma_commit_w(bar_dp);
                 BTRACE(2, i);
+                if (i + 1 < L) s_mma(i + 1, std::integral_constant<int, qn>{});
                 // dV += P^T(i) dO_i, in two query halves (h = 0: queries 0-31 and 64-95,
-                // h = 1: 32-63 and 96-127) so the first starts while the second's
-                // exponentials are still being computed
+                // h = 1: 32-63 and 96-127)
                 static_for<2>([&](auto HC) {
                     constexpr int h = decltype(HC)::value;
                     mbar_wait(&bar_p[h], i & 1);
@@ -552,25 +551,33 @@ __global__ void __launch_bounds__(kThreads, 1)
                     tc_fence_after();
                     static_for<4>([&](auto KK) {
                         constexpr int kk = (decltype(KK)::value >> 1) * 4 + h * 2 + (decltype(KK)::value & 1);
-                        constexpr uint32_t a_col = kColS + (kk >> 2) * 64 + (kk & 3) * 8;
-                        mma_ts_w<((kQ0 + st * 2 * T + T) >> 4) + mnoff(kk * 16)>(
+                        constexpr uint32_t a_col = kColDP + (kk >> 2) * 64 + (kk & 3) * 8;
+                        mma_ts_w<((kOffDO + ds * T) >> 4) + mnoff(kk * 16)>(
                             kTmem + kColDV, kTmem + a_col, dmn, Cfg::kIdAcc, (i > 0 || kk) ? 1u : 0u);
                     });
                 });
-                mma_commit_w(&bar_doempty[st]);
                 BTRACE(4, i);
+                // dK += dS^T(i) Q_i  (A = dS^T from TMEM, B = Q_i MN-major, K = 128 queries)
+                mbar_wait(bar_ds, i & 1);
+                tc_fence_after();
+                static_for<kBlk / 16>([&](auto KK) {
+                    constexpr int kk = decltype(KK)::value;
+                    constexpr uint32_t a_col = kColDP + 32 + (kk >> 2) * 64 + (kk & 3) * 8;
+                    mma_ts_w<((kOffQ + qs * T) >> 4) + mnoff(kk * 16)>(kTmem + kColDK, kTmem + a_col, dmn,
+                                                                      Cfg::kIdAcc, (i > 0 || kk) ? 1u : 0u);
+                });
+                mma_commit_w(&bar_doempty[ds]);
+                mma_commit_w(&bar_qempty[qs]);
+                BTRACE(1, i);
             };
-            for (uint32_t i = 0; i < L; i += 2) {
+            if (L > 0) s_mma(0, std::integral_constant<int, 0>{});
+            for (uint32_t i = 0; i < L; i += 6) {
                 block(i, std::integral_constant<int, 0>{});
                 if (i + 1 < L) block(i + 1, std::integral_constant<int, 1>{});
-            }
-            if (L > 0) {
-                mbar_wait(bar_ds, (L - 1) & 1);
-                tc_fence_after();
-                if ((L - 1) & 1)
-                    dk_mma(std::integral_constant<int, 1>{}, L == 1);
-                else
-                    dk_mma(std::integral_constant<int, 0>{}, L == 1);
+                if (i + 2 < L) block(i + 2, std::integral_constant<int, 2>{});
+                if (i + 3 < L) block(i + 3, std::integral_constant<int, 3>{});
+                if (i + 4 < L) block(i + 4, std::integral_constant<int, 4>{});
+                if (i + 5 < L) block(i + 5, std::integral_constant<int, 5>{});
             }
             mma_commit_w(bar_acc);
         }
@@ -582,7 +589,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint64_t krow = static_cast<uint64_t>(J) * kBlk + r;
         const float sl2 = p.scale_log2;
         for (uint32_t i = 0; i < L; ++i) {
-            const int st = i & 1;
+            const int ds = i % kDS;
             mbar_wait(bar_s, i & 1);
             if (warp == 4 && lane == 0) BTRACE(5, i);
             tc_fence_after();
@@ -590,31 +597,25 @@ __global__ void __launch_bounds__(kThreads, 1)
             tmem_ld32(kTmem + la + kColS + wg * 64, *reinterpret_cast<uint32_t(*)[32]>(sv));
             tmem_ld32(kTmem + la + kColS + wg * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(sv + 32));
             tmem_wait_ld();
-            const float4* lv = reinterpret_cast<const float4*>(vec + st * 256 + wg * 64);
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(bar_sfree);
+            // lse2 / D of this block's queries travel with dO_i
+            mbar_wait(&bar_dofull[ds], (i / kDS) & 1);
+            const float4* lv = reinterpret_cast<const float4*>(vec + ds * 256 + wg * 64);
             float pv[64];
+            const float2 sl = make_float2(sl2, sl2);
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                uint32_t pp[16];
-#pragma unroll
-                for (int c4 = 8 * h; c4 < 8 * h + 8; ++c4) {
-                    const float4 l4 = lv[c4];
-                    const float2 sl = make_float2(sl2, sl2);
-                    const float2 xa = __ffma2_rn(make_float2(__uint_as_float(sv[4 * c4]), __uint_as_float(sv[4 * c4 + 1])),
-                                                 sl, make_float2(-l4.x, -l4.y));
-                    const float2 xb = __ffma2_rn(make_float2(__uint_as_float(sv[4 * c4 + 2]), __uint_as_float(sv[4 * c4 + 3])),
-                                                 sl, make_float2(-l4.z, -l4.w));
-                    pv[4 * c4 + 0] = ex2(xa.x);
-                    pv[4 * c4 + 1] = ex2(xa.y);
-                    pv[4 * c4 + 2] = ex2(xb.x);
-                    pv[4 * c4 + 3] = ex2(xb.y);
-                    pp[2 * (c4 - 8 * h)] = pack_bf16(pv[4 * c4], pv[4 * c4 + 1]);
-                    pp[2 * (c4 - 8 * h) + 1] = pack_bf16(pv[4 * c4 + 2], pv[4 * c4 + 3]);
-                }
-                tmem_st16(kTmem + la + kColS + wg * 64 + 16 * h, pp);
-                tmem_wait_st();
-                tc_fence_before();
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&bar_p[h]);
+            for (int c4 = 0; c4 < 16; ++c4) {
+                const float4 l4 = lv[c4];
+                const float2 xa = __ffma2_rn(make_float2(__uint_as_float(sv[4 * c4]), __uint_as_float(sv[4 * c4 + 1])),
+                                             sl, make_float2(-l4.x, -l4.y));
+                const float2 xb = __ffma2_rn(make_float2(__uint_as_float(sv[4 * c4 + 2]), __uint_as_float(sv[4 * c4 + 3])),
+                                             sl, make_float2(-l4.z, -l4.w));
+                pv[4 * c4 + 0] = ex2(xa.x);
+                pv[4 * c4 + 1] = ex2(xa.y);
+                pv[4 * c4 + 2] = ex2(xb.x);
+                pv[4 * c4 + 3] = ex2(xb.y);
             }
             if ((warp == 4 || warp == 8) && lane == 0) BTRACE(warp == 4 ? 7 : 10, i);
             mbar_wait(bar_dp, i & 1);
@@ -624,7 +625,19 @@ __global__ void __launch_bounds__(kThreads, 1)
             tmem_ld32(kTmem + la + kColDP + wg * 64, *reinterpret_cast<uint32_t(*)[32]>(dp));
             tmem_ld32(kTmem + la + kColDP + wg * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(dp + 32));
             tmem_wait_ld();
-            const float4* dvv = reinterpret_cast<const float4*>(vec + st * 256 + 128 + wg * 64);
+            // P^T into the (now consumed) dP^T columns, in two query halves
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                uint32_t pp[16];
+#pragma unroll
+                for (int x = 0; x < 16; ++x) pp[x] = pack_bf16(pv[32 * h + 2 * x], pv[32 * h + 2 * x + 1]);
+                tmem_st16(kTmem + la + kColDP + wg * 64 + 16 * h, pp);
+                tmem_wait_st();
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&bar_p[h]);
+            }
+            const float4* dvv = reinterpret_cast<const float4*>(vec + ds * 256 + 128 + wg * 64);
             uint32_t pd[32];
 #pragma unroll
             for (int c4 = 0; c4 < 16; ++c4) {
@@ -638,8 +651,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                 pd[2 * c4] = pack_bf16(a.x, a.y);
                 pd[2 * c4 + 1] = pack_bf16(b.x, b.y);
             }
-            tmem_st16(kTmem + la + kColDP + wg * 64, pd);
-            tmem_st16(kTmem + la + kColDP + wg * 64 + 16, pd + 16);
+            tmem_st16(kTmem + la + kColDP + wg * 64 + 32, pd);
+            tmem_st16(kTmem + la + kColDP + wg * 64 + 48, pd + 16);
             tmem_wait_st();
             tc_fence_before();
             __syncwarp();
@@ -729,8 +742,8 @@ int launch_bwd_t(const void* q, const void* k, const void* v, const void* o, con
     if (getenv("RADIAL_BWD_DQ_ONLY")) return RADIAL_OK;  // trace builds: time the dQ kernel alone
 #endif
     {
-        const int smem = 6 * T + 2048 + 128 + 1024;
-        auto kern = radial_attn_bwd_dkdv_kernel<D>;  // 6 tiles: K, V, 2 x (Q, dO)
+        const int smem = 7 * T + 2048 + 160;  // K, V, 3 Q, 2 dO, lse2/D, barriers (no align slack)
+        auto kern = radial_attn_bwd_dkdv_kernel<D>;
         RADIAL_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         p.ptr = L->col_ptr;
         p.idx = L->row_idx;
