@@ -143,23 +143,24 @@ __global__ void __launch_bounds__(kThreads, 1)
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     constexpr int T = Cfg::kTileBytes;
-    constexpr int kKS = 3, kVS = 2;  // ring depths
-    // [dO | K0 K1 K2 | V0 V1 | barriers]
+    constexpr int kKS = 4, kVS = 2;  // ring depths (K is held from S(j) to dQ(j): deeper)
+    constexpr int kUnroll = 4;       // lcm of the ring depths: slots are compile-time constants
+    // [dO | K0..K3 | V0 V1 | barriers]
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (1 + kKS + kVS) * T);
-    uint64_t* bar_q = bars;            // Q rows stored into TMEM (8 warp arrivals)
-    uint64_t* bar_do = bars + 1;       // dO landed
-    uint64_t* bar_kfull = bars + 2;    // [3]
-    uint64_t* bar_kempty = bars + 5;   // [3] K_j free (dQ(j) done)
-    uint64_t* bar_vfull = bars + 8;    // [2]
-    uint64_t* bar_vempty = bars + 10;  // [2] V_j free (dP(j) done)
-    uint64_t* bar_s = bars + 12;       // S(j) computed
-    uint64_t* bar_dp = bars + 13;      // dP(j) computed
-    uint64_t* bar_sfree = bars + 14;   // S(j) loaded by the warpgroups (8)
-    uint64_t* bar_dpfree = bars + 15;  // dP(j) loaded (8)
-    uint64_t* bar_ds = bars + 16;      // dS(j) in TMEM (8)
-    uint64_t* bar_dsfree = bars + 17;  // dQ(j) done: dS columns free
-    uint64_t* bar_acc = bars + 18;     // dQ final
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 19);
+    uint64_t* bar_q = bars;                   // Q rows stored into TMEM (8 warp arrivals)
+    uint64_t* bar_do = bars + 1;              // dO landed
+    uint64_t* bar_kfull = bars + 2;           // [kKS]
+    uint64_t* bar_kempty = bar_kfull + kKS;   // [kKS] K_j free (dQ(j) done)
+    uint64_t* bar_vfull = bar_kempty + kKS;   // [kVS]
+    uint64_t* bar_vempty = bar_vfull + kVS;   // [kVS] V_j free (dP(j) done)
+    uint64_t* bar_s = bar_vempty + kVS;       // S(j) computed
+    uint64_t* bar_dp = bar_s + 1;             // dP(j) computed
+    uint64_t* bar_sfree = bar_s + 2;          // S(j) loaded by the warpgroups (8)
+    uint64_t* bar_dpfree = bar_s + 3;         // dP(j) loaded (8)
+    uint64_t* bar_ds = bar_s + 4;             // dS(j) in TMEM (8)
+    uint64_t* bar_dsfree = bar_s + 5;         // dQ(j) done: dS columns free
+    uint64_t* bar_acc = bar_s + 6;            // dQ final
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar_s + 7);
     constexpr uint32_t kColS = 0, kColDP = 128, kColDQ = 256, kColDS = 256 + D, kColQ = 320 + D;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -230,10 +231,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                                                                     Cfg::kIdAcc, (!first || kk) ? 1u : 0u);
                 });
             };
-            // step j: ring slots are compile-time constants (the loop is unrolled by 6 =
-            // lcm of the ring depths)
+            // step j: ring slots are compile-time constants (the loop is unrolled by kUnroll)
             auto block = [&](uint32_t j, auto PC) {
-                constexpr int P6 = decltype(PC)::value;  // == j % 6
+                constexpr int P6 = decltype(PC)::value;  // == j % kUnroll
                 constexpr int ks = P6 % kKS, vs = P6 % kVS, ksp = (P6 + kKS - 1) % kKS;
                 // S(j) = Q K_j^T  (TS: Q from TMEM)
                 mbar_wait(&bar_kfull[ks], (j / kKS) & 1);
@@ -268,22 +268,17 @@ __global__ void __launch_bounds__(kThreads, 1)
                     mma_commit_w(bar_dsfree);
                 }
             };
-            for (uint32_t j = 0; j < L; j += 6) {
-                block(j, std::integral_constant<int, 0>{});
-                if (j + 1 < L) block(j + 1, std::integral_constant<int, 1>{});
-                if (j + 2 < L) block(j + 2, std::integral_constant<int, 2>{});
-                if (j + 3 < L) block(j + 3, std::integral_constant<int, 3>{});
-                if (j + 4 < L) block(j + 4, std::integral_constant<int, 4>{});
-                if (j + 5 < L) block(j + 5, std::integral_constant<int, 5>{});
+            for (uint32_t j = 0; j < L; j += kUnroll) {
+                static_for<kUnroll>([&](auto UC) {
+                    if (j + decltype(UC)::value < L) block(j + decltype(UC)::value, UC);
+                });
             }
             if (L > 0) {
                 mbar_wait(bar_ds, (L - 1) & 1);
                 tc_fence_after();
-                switch ((L - 1) % kKS) {
-                    case 0: dq_mma(std::integral_constant<int, 0>{}, L == 1); break;
-                    case 1: dq_mma(std::integral_constant<int, 1>{}, L == 1); break;
-                    default: dq_mma(std::integral_constant<int, 2>{}, L == 1); break;
-                }
+                static_for<kKS>([&](auto KC) {
+                    if ((L - 1) % kKS == decltype(KC)::value) dq_mma(KC, L == 1);
+                });
             }
             mma_commit_w(bar_acc);
         }
@@ -729,7 +724,7 @@ int launch_bwd_t(const void* q, const void* k, const void* v, const void* o, con
     if (items > 0x7fffffffull) return fail(RADIAL_ERR_INVALID, "attn_bwd: too many work items");
     const int T = BwdCfg<D>::kTileBytes;
     {
-        const int smem = 6 * T + 256 + 1024;  // dO, 3 K + 2 V stages, barriers
+        const int smem = 7 * T + 256 + 1024;  // dO, 4 K + 2 V stages, barriers
         auto kern = radial_attn_bwd_dq_kernel<D>;
         RADIAL_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         p.ptr = L->row_ptr;
