@@ -50,7 +50,7 @@ __host__ __device__ __forceinline__ bool kept_span(const MaskParams& p, uint32_t
         case RADIAL_KIND_RADIAL: {
             const uint32_t e = d <= 1 ? 0u : floor_log2_u64(d);
             const uint64_t pw = 1ull << e;
-            if (pw <= s) return band(static_cast<uint32_t>(s / pw) - 1);
+            if (pw <= s) return band((s >> e) - 1);  // s / 2^e (e < 32 here)
             const uint64_t period = (pw + s - 1) / s;
             if (d % period == 0) {
                 lo = k_lo;
