@@ -147,9 +147,21 @@ int host_fwd(const void* q, const void* k, const void* v, void* o, float* lse, u
     auto* dv = base + 2 * tbytes;
     auto* dO = base + 3 * tbytes;
     float* dl = reinterpret_cast<float*>(base + 4 * tbytes);
-    // group size: ~6 groups (first-group latency vs per-kernel tail), at least 1 head
-    const uint32_t gh = std::max<uint32_t>(1, (heads + 5) / 6);
-    const uint32_t groups = (heads + gh - 1) / gh;
+    // head groups: a single head first and last (only their copy-in / copy-out is exposed),
+    // ~4-head groups in between (fewer per-launch tails); consecutive kernels alternate
+    // between two streams so one group's tail overlaps the next group's start
+    std::vector<uint32_t> gstart;
+    {
+        const uint32_t mid = heads > 2 ? heads - 2 : 0;
+        const uint32_t gm = std::max<uint32_t>(1, std::min<uint32_t>(4, (mid + 4) / 5));
+        uint32_t h = 0;
+        gstart.push_back(h);
+        if (heads > 1) gstart.push_back(h += 1);
+        while (h + gm < heads - (heads > 2 ? 1u : 0u)) gstart.push_back(h += gm);
+        if (heads > 2 && gstart.back() != heads - 1) gstart.push_back(heads - 1);
+        if (gstart.back() >= heads) gstart.pop_back();
+    }
+    const uint32_t groups = static_cast<uint32_t>(gstart.size());
     while (hp.ev.size() < 3 * static_cast<size_t>(groups) + 1) {
         cudaEvent_t e;
         RADIAL_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
@@ -160,7 +172,7 @@ int host_fwd(const void* q, const void* k, const void* v, void* o, float* lse, u
     RADIAL_CUDA_TRY(cudaStreamWaitEvent(hp.in, start, 0));
     const float sc = resolve_scale(scale, head_dim);
     for (uint32_t g = 0; g < groups; ++g) {
-        const uint32_t h0 = g * gh, hn = std::min(gh, heads - h0);
+        const uint32_t h0 = gstart[g], hn = (g + 1 < groups ? gstart[g + 1] : heads) - h0;
         const size_t off = hbytes * h0, len = hbytes * hn;
         cudaEvent_t e_in = hp.ev[3 * g], e_k = hp.ev[3 * g + 1], e_out = hp.ev[3 * g + 2];
         const auto* hq = static_cast<const uint8_t*>(q) + off;
