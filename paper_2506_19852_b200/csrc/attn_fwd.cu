@@ -341,16 +341,25 @@ __global__ void __launch_bounds__(kThreads, 1)
         const float sl2 = p.scale_log2;
         float m = -INFINITY, l = 0.f;
         uint32_t sphase = 0;
+        uint32_t e_next = L > 0 ? entry(0) : 0u;
 #ifdef RADIAL_LOAD_ONLY
         for (uint32_t j = 0; j < 0; ++j) {
 #else
-        uint32_t e_next = L > 0 ? entry(0) : 0u;
+#ifdef RADIAL_FWD_PINGPONG
+        if (t == 1) named_bar_arrive(1, 256);  // tile 0 takes the first turn
+#endif
         for (uint32_t j = 0; j < L; ++j) {
 #endif
             const uint32_t e = e_next;  // entry(j), loaded one iteration ahead
             if (j + 1 < L) e_next = entry(j + 1);
             const uint32_t mask = e >> 28;
-            if (((mask >> (t * Cfg::GT)) & ((1u << Cfg::GT) - 1)) == 0) continue;
+            if (((mask >> (t * Cfg::GT)) & ((1u << Cfg::GT) - 1)) == 0) {
+#ifdef RADIAL_FWD_PINGPONG
+                named_bar_sync(1 + t, 256);      // pass this block's exponential turn on
+                named_bar_arrive(2 - t, 256);
+#endif
+                continue;
+            }
             const uint32_t J = e & 0x0FFFFFFFu;
             if ((warp & 3) == 0 && lane == 0) TRACE(4 * t + 0, j);
             mbar_wait(&bar_sfull[t], sphase);
@@ -473,6 +482,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             // exponentials are still being computed.
             float2 r2a = make_float2(0.f, 0.f), r2b = make_float2(0.f, 0.f);
             const float2 sl = make_float2(sl2, sl2), nm = make_float2(-mb, -mb);
+#ifdef RADIAL_FWD_PINGPONG
+            // the two tiles take strict turns on the MUFU pipe (tile 0 first for each block)
+            named_bar_sync(1 + t, 256);
+#endif
             auto half = [&](int h, auto POLY) {
                 constexpr int NP = decltype(POLY)::value;
                 uint32_t pk[BK / 4];
@@ -512,7 +525,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                     half(h, std::integral_constant<int, 0>{});
             }
             l += (r2a.x + r2a.y) + (r2b.x + r2b.y);
+#ifdef RADIAL_FWD_PINGPONG
+            named_bar_arrive(2 - t, 256);
+#endif
         }
+#ifdef RADIAL_FWD_PINGPONG
+        if (t == 0) named_bar_sync(1, 256);  // consume tile 1's last hand-back
+#endif
         // ------------------------------------------------------------ epilogue
         mbar_wait(&bar_ofull[t], 0);
         tc_fence_after();
