@@ -186,15 +186,17 @@ int run_rate(int iters, int ctas, unsigned long long* out_dev) {
 
 // mode: bit0 TS, bit1 N=256, bit2 two accumulators; 6 / 7 = SS / TS N=64
 extern "C" int radial_cuda_debug_mma_rate(int mode, int iters, int ctas, unsigned long long* out_dev) {
-    switch (mode & 7) {
+    switch (mode) {
         case 0: return run_rate<false, 128, 1>(iters, ctas, out_dev);
         case 1: return run_rate<true, 128, 1>(iters, ctas, out_dev);
         case 2: return run_rate<false, 256, 1>(iters, ctas, out_dev);
         case 3: return run_rate<true, 256, 1>(iters, ctas, out_dev);
         case 4: return run_rate<false, 128, 2>(iters, ctas, out_dev);
         case 5: return run_rate<true, 128, 2>(iters, ctas, out_dev);
-        case 6: return run_rate<false, 64, 1>(iters, ctas, out_dev);
-        case 7: return run_rate<true, 64, 1>(iters, ctas, out_dev);
+        case 6: return run_rate<false, 64, 2>(iters, ctas, out_dev);
+        case 7: return run_rate<true, 64, 2>(iters, ctas, out_dev);
+        case 8: return run_rate<false, 64, 1>(iters, ctas, out_dev);
+        case 9: return run_rate<true, 64, 1>(iters, ctas, out_dev);
         default: return RADIAL_ERR_INVALID;
     }
 }
