@@ -183,6 +183,57 @@ def test_paper_scale_hunyuan33_sampled_blocks(P):
         assert_within(block_errors(got, want, rows, B), f"H33 head {h}")
 
 
+@pytest.mark.parametrize("f,s,H", [(21, 3600, 40), (28, 1590, 24), (132, 3600, 24)],
+                         ids=["wan21", "mochi28", "hunyuan132"])
+def test_paper_scale_other_configs_sampled_blocks(P, f, s, H):
+    """BASELINE configs[2..4] at full size (W21 40 heads, M28, the 475k-token H132): every
+    head on the GPU, a sample of (head, query block) pairs against the fp64 oracle; the
+    H132 lse is checked too (the backward consumes it)."""
+    import torch
+    B, d = 128, 128
+    n = f * s
+    g = torch.Generator(device="cuda").manual_seed(99)
+    q = torch.randn(H, n, d, device="cuda", generator=g).to(torch.bfloat16)
+    k = torch.randn(H, n, d, device="cuda", generator=g).to(torch.bfloat16)
+    v = torch.randn(H, n, d, device="cuda", generator=g).to(torch.bfloat16)
+    lay = P.device_layout(P.GridShape(f, s), P.PatternSpec.radial(), B)
+    o, lse = P.masked_attention(q, k, v, lay, return_lse=True)
+    torch.cuda.synchronize()
+    host = lay.host()
+    R = host.grid_rows
+    rng = np.random.default_rng(f)
+    for h in (0, H - 1):
+        blocks = sorted({0, R // 3, R - 1} | set(rng.integers(0, R, 2).tolist()))
+        rows = np.concatenate([np.arange(I * B, min(n, (I + 1) * B)) for I in blocks])
+        qh, kh, vh = (x[h].float().cpu().numpy() for x in (q, k, v))
+        want, want_lse = O.attention_rows(qh, kh, vh, B, host.row_ptr, host.col_idx, rows, want_lse=True)
+        got = o[h].float().cpu().numpy()[rows]
+        assert_within(block_errors(got, want, rows, B), f"f{f} s{s} head {h}")
+        np.testing.assert_allclose(lse[h].cpu().numpy()[rows], want_lse, rtol=0, atol=2e-3)
+    del q, k, v, o, lse
+    torch.cuda.empty_cache()
+
+
+def test_paper_scale_dense_comparator_sampled_rows(P):
+    """K4 at the M28 shape (44,520 tokens, every key): sampled query blocks of two heads
+    against the fp64 dense oracle (the reference's dense_attention, attention.hpp:141-163)."""
+    import torch
+    f, s, B, d, H = 28, 1590, 128, 128, 4
+    n = f * s
+    g = torch.Generator(device="cuda").manual_seed(7)
+    q, k, v = (torch.randn(H, n, d, device="cuda", generator=g).to(torch.bfloat16) for _ in range(3))
+    o = P.dense_attention(q, k, v, block_size=B)
+    torch.cuda.synchronize()
+    R = (n + B - 1) // B
+    for h in (0, H - 1):
+        blocks = [0, R // 2, R - 1]
+        rows = np.concatenate([np.arange(I * B, min(n, (I + 1) * B)) for I in blocks])
+        qh, kh, vh = (x[h].float().cpu().numpy() for x in (q, k, v))
+        want = O.attention_rows(qh, kh, vh, B, None, None, rows)
+        got = o[h].float().cpu().numpy()[rows]
+        assert_within(block_errors(got, want, rows, B), f"dense M28 head {h}")
+
+
 @pytest.mark.parametrize("f,s,B,d,kind,sink,tw,sw", [
     (8, 256, 64, 64, "radial", True, 0, 0), (6, 300, 128, 128, "radial", False, 0, 0),
     (33, 150, 128, 128, "radial", True, 0, 0), (5, 333, 64, 128, "sta", True, 1, 40),
