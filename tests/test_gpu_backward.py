@@ -88,12 +88,15 @@ def test_backward_matches_torch_autograd_dense_mask(P):
     assert rel_o < 1e-2
 
 
-def test_backward_mochi28_full_shape_sampled(P):
-    """BASELINE configs[3] (Mochi-1 28 x 1590, 24 heads, d 128) at full size: all heads on
-    the GPU; sampled query blocks (dQ) and KV blocks (dK, dV) -- sink column, tail, random --
+@pytest.mark.parametrize("f,s,heads_checked", [(28, 1590, (0, 17)), (132, 3600, (5,))],
+                         ids=["mochi28", "hunyuan132"])
+def test_backward_full_shape_sampled(P, f, s, heads_checked):
+    """BASELINE configs[3] (Mochi-1 28 x 1590) and configs[4] (HunyuanVideo 4x length
+    extension, 132 x 3600 = 475k tokens), 24 heads, d 128, at full size: all heads on the
+    GPU; sampled query blocks (dQ) and KV blocks (dK, dV) -- sink column, tail, random --
     against a torch fp32 restatement of the gradients over exactly the kept blocks."""
     import torch
-    f, s, d, H, B = 28, 1590, 128, 24, 128
+    d, H, B = 128, 24, 128
     n = f * s
     g = torch.Generator(device="cuda").manual_seed(11)
     q, k, v, do = (torch.randn(H, n, d, device="cuda", generator=g).to(torch.bfloat16) for _ in range(4))
@@ -112,7 +115,7 @@ def test_backward_mochi28_full_shape_sampled(P):
     def keys_of(lst):
         return torch.cat([rows_of(int(J)) for J in lst])
 
-    for h in (0, 17):
+    for h in heads_checked:
         qf, kf, vf, dof = (x[h].float() for x in (q, k, v, do))
         # fp32 row statistics (lse, D) for any query block, restated from the forward
         def stats(I):
