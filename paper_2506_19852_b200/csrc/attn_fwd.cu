@@ -491,6 +491,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                 uint32_t pk[BK / 4];
 #pragma unroll
                 for (int c = h * (BK / 2); c < (h + 1) * (BK / 2); c += 2) {
+                    // store each 32-column group of P as soon as it is packed, so its
+                    // tcgen05.st latency overlaps the next group's exponentials
+                    if (c > h * (BK / 2) && (c - h * (BK / 2)) % 32 == 0)
+                        tmem_st16(s_addr + h * (BK / 4) + (c - h * (BK / 2)) / 2 - 16,
+                                  pk + (c - h * (BK / 2)) / 2 - 16);
                     const float2 x = __ffma2_rn(make_float2(s[c], s[c + 1]), sl, nm);
                     float2 pr;
                     if (((c >> 1) & 3) < NP) {
@@ -509,8 +514,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         r2a = __fadd2_rn(r2a, pr);
                     pk[(c - h * (BK / 2)) / 2] = pack_bf16(pr.x, pr.y);
                 }
-#pragma unroll
-                for (int c = 0; c < BK / 4; c += 16) tmem_st16(s_addr + h * (BK / 4) + c, pk + c);
+                tmem_st16(s_addr + h * (BK / 4) + BK / 4 - 16, pk + BK / 4 - 16);
                 tmem_wait_st();
                 tc_fence_before();
                 __syncwarp();
