@@ -195,13 +195,6 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const uint32_t slot = t % kSlots;
                 mbar_wait(&bar_empty[slot], ((t / kSlots) & 1) ^ 1);
                 TRACE(18 + (t & 1), t >> 1);
-#ifdef RADIAL_SKIP_LOADS  // timing experiment only: 1 = no V loads, 2 = no K/V loads after the first ring
-                if (((RADIAL_SKIP_LOADS & 1) && (t & 1) && t >= 2 * kSlots) ||
-                    ((RADIAL_SKIP_LOADS & 2) && t >= 2 * kSlots)) {
-                    mbar_arrive(&bar_full[slot]);
-                    continue;
-                }
-#endif
                 mbar_arrive_expect_tx(&bar_full[slot], Cfg::kKVBytes);
                 uint8_t* dst = smem + Cfg::kSmemKV + slot * Cfg::kKVBytes;
                 const CUtensorMap* tm = (t & 1) ? &tm_v : &tm_k;
@@ -253,9 +246,6 @@ __global__ void __launch_bounds__(kThreads, 1)
                 tc_fence_after();
                 auto pv = [&](auto TC, uint32_t& acc, uint32_t& pphase) {
                     constexpr int T = decltype(TC)::value;
-#ifdef RADIAL_LOAD_ONLY  // timing experiment only: K/V streaming without MMAs or softmax
-                    return;
-#endif
                     constexpr uint32_t p_col = T ? Cfg::kColS1 : Cfg::kColS0;
                     constexpr uint32_t o_col = T ? Cfg::kColO1 : Cfg::kColO0;
 
@@ -275,9 +265,6 @@ __global__ void __launch_bounds__(kThreads, 1)
                 };
                 auto qk = [&](auto TC) {
                     constexpr int T = decltype(TC)::value;
-#ifdef RADIAL_LOAD_ONLY
-                    return;
-#endif
                     constexpr uint32_t s_col = T ? Cfg::kColS1 : Cfg::kColS0;
 
                     static_for<D / 16>([&](auto KC) {
@@ -342,24 +329,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         float m = -INFINITY, l = 0.f;
         uint32_t sphase = 0;
         uint32_t e_next = L > 0 ? entry(0) : 0u;
-#ifdef RADIAL_LOAD_ONLY
-        for (uint32_t j = 0; j < 0; ++j) {
-#else
-#ifdef RADIAL_FWD_PINGPONG
-        if (t == 1) named_bar_arrive(1, 256);  // tile 0 takes the first turn
-#endif
         for (uint32_t j = 0; j < L; ++j) {
-#endif
             const uint32_t e = e_next;  // entry(j), loaded one iteration ahead
             if (j + 1 < L) e_next = entry(j + 1);
             const uint32_t mask = e >> 28;
-            if (((mask >> (t * Cfg::GT)) & ((1u << Cfg::GT) - 1)) == 0) {
-#ifdef RADIAL_FWD_PINGPONG
-                named_bar_sync(1 + t, 256);      // pass this block's exponential turn on
-                named_bar_arrive(2 - t, 256);
-#endif
-                continue;
-            }
+            if (((mask >> (t * Cfg::GT)) & ((1u << Cfg::GT) - 1)) == 0) continue;
             const uint32_t J = e & 0x0FFFFFFFu;
             if ((warp & 3) == 0 && lane == 0) TRACE(4 * t + 0, j);
             mbar_wait(&bar_sfull[t], sphase);
@@ -482,10 +456,6 @@ __global__ void __launch_bounds__(kThreads, 1)
             // exponentials are still being computed.
             float2 r2a = make_float2(0.f, 0.f), r2b = make_float2(0.f, 0.f);
             const float2 sl = make_float2(sl2, sl2), nm = make_float2(-mb, -mb);
-#ifdef RADIAL_FWD_PINGPONG
-            // the two tiles take strict turns on the MUFU pipe (tile 0 first for each block)
-            named_bar_sync(1 + t, 256);
-#endif
             auto half = [&](int h, auto POLY) {
                 constexpr int NP = decltype(POLY)::value;
                 uint32_t pk[BK / 4];
@@ -501,12 +471,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                     if (((c >> 1) & 3) < NP) {
                         pr = ex2_poly2(x);  // FA4-style FMA-pipe exp2 for a share of columns
                     } else {
-#ifdef RADIAL_FAKE_EXP  // timing experiment only: no MUFU work (wrong results)
-                        pr = x;
-#else
                         pr.x = ex2(x.x);
                         pr.y = ex2(x.y);
-#endif
                     }
                     if ((c >> 1) & 1)
                         r2b = __fadd2_rn(r2b, pr);
@@ -529,13 +495,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     half(h, std::integral_constant<int, 0>{});
             }
             l += (r2a.x + r2a.y) + (r2b.x + r2b.y);
-#ifdef RADIAL_FWD_PINGPONG
-            named_bar_arrive(2 - t, 256);
-#endif
         }
-#ifdef RADIAL_FWD_PINGPONG
-        if (t == 0) named_bar_sync(1, 256);  // consume tile 1's last hand-back
-#endif
         // ------------------------------------------------------------ epilogue
         mbar_wait(&bar_ofull[t], 0);
         tc_fence_after();
