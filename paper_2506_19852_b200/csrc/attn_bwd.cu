@@ -24,6 +24,13 @@
 #include "radial_internal.h"
 #include "sm100.cuh"
 
+// setmaxnreg split: producer/MMA warpgroup vs elementwise warpgroups (384 threads x 168 =
+// 128 x LO + 256 x HI must hold)
+#ifndef RADIAL_REGS_LO
+#define RADIAL_REGS_LO 104
+#define RADIAL_REGS_HI 200
+#endif
+
 using namespace radial_sm100;
 
 namespace radial_detail {
@@ -196,7 +203,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (*tmem_slot != 0) __trap();
 
     if (warp < 4) {
-        regs_dec<104>();
+        regs_dec<RADIAL_REGS_LO>();
         if (warp == 0 && lane == 0) {
             // ------------------------------------------------ producer
             mbar_arrive_expect_tx(bar_do, T);
@@ -283,7 +290,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             mma_commit_w(bar_acc);
         }
     } else {
-        regs_inc<200>();
+        regs_inc<RADIAL_REGS_HI>();
         // ---------------------------------------------------- elementwise
         const int wg = (warp - 4) >> 2;  // key columns [64 wg, 64 wg + 64)
         const int r = ((warp & 3) << 5) + lane;
@@ -476,7 +483,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     constexpr uint32_t kColS = 0, kColDP = 128, kColDV = 256, kColDK = 384;
 
     if (warp < 4) {
-        regs_dec<104>();
+        regs_dec<RADIAL_REGS_LO>();
         if (warp == 0 && lane == 0) {
             // ------------------------------------------------ producer
             mbar_arrive_expect_tx(bar_res, 2 * T);
@@ -577,7 +584,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             mma_commit_w(bar_acc);
         }
     } else {
-        regs_inc<200>();
+        regs_inc<RADIAL_REGS_HI>();
         const int wg = (warp - 4) >> 2;  // query columns [64 wg, 64 wg + 64)
         const int r = ((warp & 3) << 5) + lane;  // key row of the tile
         const uint32_t la = static_cast<uint32_t>((warp & 3) * 32) << 16;

@@ -28,6 +28,13 @@
 #include "radial_internal.h"
 #include "sm100.cuh"
 
+// setmaxnreg split: producer/MMA warpgroup vs elementwise warpgroups (384 threads x 168 =
+// 128 x LO + 256 x HI must hold)
+#ifndef RADIAL_REGS_LO
+#define RADIAL_REGS_LO 104
+#define RADIAL_REGS_HI 200
+#endif
+
 using namespace radial_sm100;
 
 #ifdef RADIAL_TRACE
@@ -181,7 +188,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // producer / MMA / allocator warpgroup needs few registers; the two softmax
     // warpgroups hold a 128-column S row each (384 x 168 = 128 x 104 + 256 x 200)
     if (warp < 4) {
-        regs_dec<104>();
+        regs_dec<RADIAL_REGS_LO>();
     if (warp == 0) {
         // ------------------------------------------------------------ producer
         if (lane == 0) {
@@ -313,7 +320,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
     }
     } else {
-        regs_inc<200>();
+        regs_inc<RADIAL_REGS_HI>();
         // ------------------------------------------------------------ softmax
         const int t = (warp - 4) >> 2;                 // Q tile
         const int r = ((warp & 3) << 5) + lane;        // row in tile = TMEM lane
