@@ -80,7 +80,7 @@ constexpr float kRescaleThreshold = 8.0f;  // log2 units
 #ifndef RADIAL_POLY_PAIRS
 #define RADIAL_POLY_PAIRS 0  // measured on B200: MUFU-only is fastest with the current pipeline
 #endif
-constexpr int kPolyPairs = RADIAL_POLY_PAIRS;  // column pairs per 4 using the polynomial exp2
+constexpr int kPolyPairs = RADIAL_POLY_PAIRS;  // column pairs per 8 using the polynomial exp2
 
 struct FwdParams {
     __nv_bfloat16* o;
@@ -475,7 +475,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                                   pk + (c - h * (BK / 2)) / 2 - 16);
                     const float2 x = __ffma2_rn(make_float2(s[c], s[c + 1]), sl, nm);
                     float2 pr;
-                    if (((c >> 1) & 3) < NP) {
+                    if (((c >> 1) & 7) < NP) {
                         pr = ex2_poly2(x);  // FA4-style FMA-pipe exp2 for a share of columns
                     } else {
                         pr.x = ex2(x.x);

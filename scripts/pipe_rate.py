@@ -23,6 +23,16 @@ def main():
             instr = iters * 8 * warps  # warp-instructions per SM
             print(f"warps/SM={warps:3d} {NAMES[op]:18s}: {instr / cyc:6.2f} warp-instr/clk/SM = {32 * instr / cyc:6.1f} lanes/clk/SM")
 
+    # softmax exp phase: clk per column pair per warp, MUFU vs polynomial share
+    for warps in (4, 8):
+        for np_ in (0, 1, 2, 3, 4, 8):
+            iters = 256
+            assert lib.radial_cuda_debug_exp_phase(np_, iters, warps, ctypes.c_void_p(out.data_ptr())) == 0
+            cyc = (out & ((1 << 62) - 1)).double().mean().item()
+            per_pair = cyc / (iters * 64) / (warps / 4)  # per warp sharing a sub-partition
+            print(f"exp phase warps/SM={warps} poly {np_}/8: {cyc / (iters * 64):7.2f} clk per pair-iteration "
+                  f"({per_pair:6.2f} per pair per warp-slot)")
+
 
 if __name__ == "__main__":
     main()
