@@ -33,10 +33,20 @@ __device__ __forceinline__ bool mbar_try_wait(uint32_t bar, uint32_t parity) {
     uint32_t ok;
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
+#ifndef RADIAL_MBAR_HINT
+#define RADIAL_MBAR_HINT 1000000  // ns; 0 = no hint (measured: +0.8% forward, backward unchanged)
+#endif
+#if RADIAL_MBAR_HINT  // suspend-time hint: waiting threads sleep until the phase flips instead of spinning
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+#else
         "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+#endif
         "selp.u32 %0, 1, 0, p;\n\t}"
         : "=r"(ok)
         : "r"(bar), "r"(parity)
+#if RADIAL_MBAR_HINT
+          , "n"(RADIAL_MBAR_HINT)
+#endif
         : "memory");
     return ok != 0;
 }
