@@ -148,12 +148,15 @@ int host_fwd(const void* q, const void* k, const void* v, void* o, float* lse, u
     auto* dO = base + 3 * tbytes;
     float* dl = reinterpret_cast<float*>(base + 4 * tbytes);
     // head groups: a single head first and last (only their copy-in / copy-out is exposed),
-    // ~4-head groups in between (fewer per-launch tails); consecutive kernels alternate
+    // groups of up to RADIAL_HOST_GROUP_MAX heads in between; consecutive kernels alternate
     // between two streams so one group's tail overlaps the next group's start
     std::vector<uint32_t> gstart;
     {
         const uint32_t mid = heads > 2 ? heads - 2 : 0;
-        const uint32_t gm = std::max<uint32_t>(1, std::min<uint32_t>(4, (mid + 4) / 5));
+#ifndef RADIAL_HOST_GROUP_MAX  // measured at H33: 1 head per group 70.0 ms, 2: 70.1, 4: 72.4
+#define RADIAL_HOST_GROUP_MAX 1
+#endif
+        const uint32_t gm = std::max<uint32_t>(1, std::min<uint32_t>(RADIAL_HOST_GROUP_MAX, (mid + 4) / 5));
         uint32_t h = 0;
         gstart.push_back(h);
         if (heads > 1) gstart.push_back(h += 1);
