@@ -55,14 +55,17 @@ constexpr int kTraceCtas = 4, kTraceSteps = 64, kTraceEv = 24;
 
 namespace {
 
-// MMA issue from lane 0 of warp 1 (measured 2-3% faster here than the warp-converged
-// elect.sync issue the backward kernels use; build with -DRADIAL_FWD_WARP_MMA to compare)
-#ifndef RADIAL_FWD_WARP_MMA
-#define RADIAL_FWD_LANE0 1
+// MMA issue: warp 1 runs converged and elect.sync picks the issuing lane inside the asm;
+// the S and PV MMAs are issued four K-steps per asm block (mma_ss_x4 / mma_ts_x4), so ptxas
+// emits back-to-back UTCHMMA (+0.8% per clock over single-lane issue, which costs ~16
+// instructions per MMA on the sub-partition the MMA warp shares with two softmax warps).
+// -DRADIAL_FWD_LANE0 builds the single-lane variant for comparison.
+#ifdef RADIAL_FWD_LANE0
 #define FWD_MMA_SS mma_ss_off
 #define FWD_MMA_TS mma_ts_off
 #define FWD_COMMIT mma_commit
 #else
+#define RADIAL_FWD_WARP_MMA 1
 #define FWD_MMA_SS mma_ss_w
 #define FWD_MMA_TS mma_ts_w
 #define FWD_COMMIT mma_commit_w
@@ -231,7 +234,16 @@ __global__ void __launch_bounds__(kThreads, 1)
             bool pend0 = false, pend1 = false;
             uint32_t acc0 = 0, acc1 = 0;
             uint32_t pphase0 = 0, pphase1 = 0;
-            uint32_t e_next = L > 0 ? entry(0) : 0u;
+            // warp-converged issue: broadcast lane 0's value so the compiler sees a uniform
+            // operand for every branch on it (no divergent / waterfall code paths)
+            auto uentry = [&](uint32_t j) -> uint32_t {
+#ifdef RADIAL_FWD_LANE0
+                return entry(j);
+#else
+                return __shfl_sync(0xffffffffu, entry(j), 0);
+#endif
+            };
+            uint32_t e_next = L > 0 ? uentry(0) : 0u;
             // step j: PV_A(j-1), S_A(j), PV_B(j-1), S_B(j); each operand is waited for just
             // before its first use and released right after its last use.
             auto step = [&](uint32_t j, auto PC) {
@@ -241,7 +253,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 uint32_t tf0 = 0, tf1 = 0;
                 if (j < L) {
                     const uint32_t m = e_next >> 28;  // entry(j), loaded one step ahead
-                    if (j + 1 < L) e_next = entry(j + 1);
+                    if (j + 1 < L) e_next = uentry(j + 1);
                     tf0 = m & ((1u << Cfg::GT) - 1);
                     tf1 = (m >> Cfg::GT) & ((1u << Cfg::GT) - 1);
                 }
@@ -261,6 +273,14 @@ __global__ void __launch_bounds__(kThreads, 1)
                         mbar_wait(&bar_pready[2 * T + h], pphase);
                         TRACE(8 + 2 * T + h, j - 1);
                         tc_fence_after();
+#if defined(RADIAL_FWD_WARP_MMA) && !defined(RADIAL_FWD_NO_GROUP)
+                        if constexpr (BK / 32 == 4) {
+                            // four K-steps per asm block (elected issue, no per-MMA overhead)
+                            constexpr int kk0 = h * 4;
+                            mma_ts_x4<((VSL * Cfg::kKVBytes + kk0 * 16 * 128) >> 4), 128>(
+                                kTmem + o_col, kTmem + p_col + kk0 * 8, dv, Cfg::kIdescO, (acc | kk0) ? 1u : 0u);
+                        } else
+#endif
                         static_for<BK / 32>([&](auto KI) {
                             constexpr int kk = h * (BK / 32) + decltype(KI)::value;
                             FWD_MMA_TS<((VSL * Cfg::kKVBytes + kk * 16 * 128) >> 4)>(
@@ -274,6 +294,15 @@ __global__ void __launch_bounds__(kThreads, 1)
                     constexpr int T = decltype(TC)::value;
                     constexpr uint32_t s_col = T ? Cfg::kColS1 : Cfg::kColS0;
 
+#if defined(RADIAL_FWD_WARP_MMA) && !defined(RADIAL_FWD_NO_GROUP)
+                    // one asm block per 64-column atom of d: four K-steps each
+                    static_for<Cfg::kAtoms>([&](auto AC) {
+                        constexpr int at = decltype(AC)::value;
+                        mma_ss_x4<((T * Cfg::kQBytes + at * Cfg::kQAtomBytes) >> 4),
+                                  ((KSL * Cfg::kKVBytes + at * Cfg::kKVAtomBytes) >> 4)>(
+                            kTmem + s_col, dq, dk, Cfg::kIdescS, at ? 1u : 0u);
+                    });
+#else
                     static_for<D / 16>([&](auto KC) {
                         constexpr int kk = decltype(KC)::value;
                         constexpr uint32_t off_q = (kk >> 2) * Cfg::kQAtomBytes + (kk & 3) * 32;
@@ -281,6 +310,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         FWD_MMA_SS<((T * Cfg::kQBytes + off_q) >> 4), ((KSL * Cfg::kKVBytes + off_k) >> 4)>(
                             kTmem + s_col, dq, dk, Cfg::kIdescS, kk ? 1u : 0u);
                     });
+#endif
                     FWD_COMMIT(&bar_sfull[T]);
                     TRACE(12 + T, j);
                 };
