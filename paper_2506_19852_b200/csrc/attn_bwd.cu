@@ -232,11 +232,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             // dQ += dS(j) K_j  (A = dS from TMEM, B = K_j MN-major, K = 128 keys)
             auto dq_mma = [&](auto KSC, bool first) {
                 constexpr int ks = decltype(KSC)::value;
-                static_for<kBlk / 16>([&](auto KK) {
-                    constexpr int kk = decltype(KK)::value;
-                    mma_ts_w<(((1 + ks) * T) >> 4) + mnoff(kk * 16)>(kTmem + kColDQ, kTmem + kColDS + kk * 8, dmn,
-                                                                    Cfg::kIdAcc, (!first || kk) ? 1u : 0u);
-                });
+                // 8 K-steps (16 keys each) as two groups of four (grouped elected issue)
+                mma_ts_x4<(((1 + ks) * T) >> 4) + mnoff(0), mnoff(16)>(kTmem + kColDQ, kTmem + kColDS, dmn,
+                                                                      Cfg::kIdAcc, first ? 0u : 1u);
+                mma_ts_x4<(((1 + ks) * T) >> 4) + mnoff(64), mnoff(16)>(kTmem + kColDQ, kTmem + kColDS + 32, dmn,
+                                                                       Cfg::kIdAcc, 1u);
             };
             // step j: ring slots are compile-time constants (the loop is unrolled by kUnroll)
             auto block = [&](uint32_t j, auto PC) {
@@ -246,10 +246,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                 mbar_wait(&bar_kfull[ks], (j / kKS) & 1);
                 if (j > 0) mbar_wait(bar_sfree, (j - 1) & 1);
                 tc_fence_after();
-                static_for<D / 16>([&](auto KK) {
-                    constexpr int kk = decltype(KK)::value;
-                    mma_ts_w<koff(kk, 0) + (((1 + ks) * T) >> 4)>(kTmem + kColS, kTmem + kColQ + kk * 8, dkm,
-                                                                   Cfg::kIdAcc128, kk ? 1u : 0u);
+                static_for<Cfg::kAtoms>([&](auto AC) {
+                    constexpr int at = decltype(AC)::value;  // four K-steps per 64-column atom of d
+                    mma_ts_x4<koff(4 * at, 0) + (((1 + ks) * T) >> 4), 2>(kTmem + kColS, kTmem + kColQ + 32 * at, dkm,
+                                                                          Cfg::kIdAcc128, at ? 1u : 0u);
                 });
                 mma_commit_w(bar_s);
                 BTRACE(1, j);
@@ -257,10 +257,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                 mbar_wait(&bar_vfull[vs], (j / kVS) & 1);
                 if (j > 0) mbar_wait(bar_dpfree, (j - 1) & 1);
                 tc_fence_after();
-                static_for<D / 16>([&](auto KK) {
-                    constexpr int kk = decltype(KK)::value;
-                    mma_ss_w<koff(kk, 0), koff(kk, 0) + (((1 + kKS + vs) * T) >> 4)>(kTmem + kColDP, dkm, dkm,
-                                                                                   Cfg::kIdAcc128, kk ? 1u : 0u);
+                static_for<Cfg::kAtoms>([&](auto AC) {
+                    constexpr int at = decltype(AC)::value;
+                    mma_ss_x4<koff(4 * at, 0), koff(4 * at, 0) + (((1 + kKS + vs) * T) >> 4)>(kTmem + kColDP, dkm, dkm,
+                                                                                             Cfg::kIdAcc128, at ? 1u : 0u);
                 });
                 mma_commit_w(bar_dp);
                 mma_commit_w(&bar_vempty[vs]);
@@ -521,10 +521,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                 mbar_wait(&bar_qfull[qs], (i / kQS) & 1);
                 if (i > 0) mbar_wait(bar_sfree, (i - 1) & 1);
                 tc_fence_after();
-                static_for<D / 16>([&](auto KK) {
-                    constexpr int kk = decltype(KK)::value;
-                    mma_ss_w<koff(kk, 0) + (kK >> 4), koff(kk, 0) + ((kOffQ + qs * T) >> 4)>(
-                        kTmem + kColS, dkm, dkm, Cfg::kIdAcc128, kk ? 1u : 0u);
+                static_for<Cfg::kAtoms>([&](auto AC) {
+                    constexpr int at = decltype(AC)::value;
+                    mma_ss_x4<koff(4 * at, 0) + (kK >> 4), koff(4 * at, 0) + ((kOffQ + qs * T) >> 4)>(
+                        kTmem + kColS, dkm, dkm, Cfg::kIdAcc128, at ? 1u : 0u);
                 });
                 mma_commit_w(bar_s);
                 BTRACE(0, i);
@@ -536,10 +536,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                 // dP^T(i) = V dO_i^T
                 mbar_wait(&bar_dofull[ds], (i / kDS) & 1);
                 tc_fence_after();
-                static_for<D / 16>([&](auto KK) {
-                    constexpr int kk = decltype(KK)::value;
-                    mma_ss_w<koff(kk, 0) + (kV >> 4), koff(kk, 0) + ((kOffDO + ds * T) >> 4)>(
-                        kTmem + kColDP, dkm, dkm, Cfg::kIdAcc128, kk ? 1u : 0u);
+                static_for<Cfg::kAtoms>([&](auto AC) {
+                    constexpr int at = decltype(AC)::value;
+                    mma_ss_x4<koff(4 * at, 0) + (kV >> 4), koff(4 * at, 0) + ((kOffDO + ds * T) >> 4)>(
+                        kTmem + kColDP, dkm, dkm, Cfg::kIdAcc128, at ? 1u : 0u);
                 });
                 mma_commit_w(bar_dp);
                 BTRACE(2, i);
@@ -562,12 +562,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                 // dK += dS^T(i) Q_i  (A = dS^T from TMEM, B = Q_i MN-major, K = 128 queries)
                 mbar_wait(bar_ds, i & 1);
                 tc_fence_after();
-                static_for<kBlk / 16>([&](auto KK) {
-                    constexpr int kk = decltype(KK)::value;
-                    constexpr uint32_t a_col = kColDP + 32 + (kk >> 2) * 64 + (kk & 3) * 8;
-                    mma_ts_w<((kOffQ + qs * T) >> 4) + mnoff(kk * 16)>(kTmem + kColDK, kTmem + a_col, dmn,
-                                                                      Cfg::kIdAcc, (i > 0 || kk) ? 1u : 0u);
-                });
+                // queries 0-63 (warpgroup 0's dS^T columns), then 64-127 (warpgroup 1's)
+                mma_ts_x4<((kOffQ + qs * T) >> 4) + mnoff(0), mnoff(16)>(kTmem + kColDK, kTmem + kColDP + 32, dmn,
+                                                                        Cfg::kIdAcc, i > 0 ? 1u : 0u);
+                mma_ts_x4<((kOffQ + qs * T) >> 4) + mnoff(64), mnoff(16)>(kTmem + kColDK, kTmem + kColDP + 96, dmn,
+                                                                         Cfg::kIdAcc, 1u);
                 mma_commit_w(&bar_doempty[ds]);
                 mma_commit_w(&bar_qempty[qs]);
                 BTRACE(1, i);
