@@ -551,12 +551,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                     mbar_wait(&bar_p[h], i & 1);
                     if (h == 0) BTRACE(3, i);
                     tc_fence_after();
-                    static_for<4>([&](auto KK) {
-                        constexpr int kk = (decltype(KK)::value >> 1) * 4 + h * 2 + (decltype(KK)::value & 1);
-                        constexpr uint32_t a_col = kColDP + (kk >> 2) * 64 + (kk & 3) * 8;
-                        mma_ts_w<((kOffDO + ds * T) >> 4) + mnoff(kk * 16)>(
-                            kTmem + kColDV, kTmem + a_col, dmn, Cfg::kIdAcc, (i > 0 || kk) ? 1u : 0u);
-                    });
+                    // K-steps 2h, 2h+1 (warpgroup 0's queries), then 4+2h, 5+2h (warpgroup 1's)
+                    mma_ts_x2<((kOffDO + ds * T) >> 4) + mnoff(32 * h), mnoff(16)>(
+                        kTmem + kColDV, kTmem + kColDP + 16 * h, dmn, Cfg::kIdAcc, (i > 0 || h) ? 1u : 0u);
+                    mma_ts_x2<((kOffDO + ds * T) >> 4) + mnoff(64 + 32 * h), mnoff(16)>(
+                        kTmem + kColDV, kTmem + kColDP + 64 + 16 * h, dmn, Cfg::kIdAcc, 1u);
                 });
                 BTRACE(4, i);
                 // dK += dS^T(i) Q_i  (A = dS^T from TMEM, B = Q_i MN-major, K = 128 queries)

@@ -245,6 +245,21 @@ __device__ __forceinline__ void mma_ts_x4(uint32_t d_tmem, uint32_t a_tmem, uint
         "r"(a_tmem), "l"(b_base), "r"(idesc), "r"(acc), "n"(OB), "n"(BSTEP)
         : "memory");
 }
+// Two K-steps of TS MMAs (A from TMEM columns a_tmem, a_tmem + 8; B = base + OB, + BSTEP).
+template <uint32_t OB, uint32_t BSTEP>
+__device__ __forceinline__ void mma_ts_x2(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_base,
+                                          uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred e, p, t;\n\t.reg .b64 b;\n\t.reg .b32 a;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\tsetp.eq.b32 t, 0, 0;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "add.s64 b, %2, %5;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], b, %3, p;\n\t"
+        "add.u32 a, %1, 8;\n\tadd.s64 b, %2, %5+%6;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a], b, %3, t;\n\t}" ::"r"(d_tmem),
+        "r"(a_tmem), "l"(b_base), "r"(idesc), "r"(acc), "n"(OB), "n"(BSTEP)
+        : "memory");
+}
 // Warp-converged tcgen05.commit (one elected lane arrives).
 __device__ __forceinline__ void mma_commit_w(uint64_t* bar) {
     asm volatile(
