@@ -30,9 +30,9 @@
 
 // setmaxnreg split: producer/MMA warpgroup vs elementwise warpgroups (384 threads x 168 =
 // 128 x LO + 256 x HI must hold)
-#ifndef RADIAL_REGS_LO
-#define RADIAL_REGS_LO 104
-#define RADIAL_REGS_HI 200
+#ifndef RADIAL_FWD_REGS_LO
+#define RADIAL_FWD_REGS_LO 72
+#define RADIAL_FWD_REGS_HI 216
 #endif
 
 using namespace radial_sm100;
@@ -188,10 +188,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     // starts at lane 0 / column 0; the constant base keeps tcgen05 operands uniform.
     if (*tmem_slot != 0) __trap();
     constexpr uint32_t tmem = kTmem;
-    // producer / MMA / allocator warpgroup needs few registers; the two softmax
-    // warpgroups hold a 128-column S row each (384 x 168 = 128 x 104 + 256 x 200)
+    // producer / MMA / allocator warpgroup needs few registers (the grouped MMA issue keeps
+    // its operands in uniform registers); the two softmax warpgroups hold a 128-column S row
+    // each (128 x 72 + 256 x 216 <= 64K; measured +1% over 104 / 200, no spills)
     if (warp < 4) {
-        regs_dec<RADIAL_REGS_LO>();
+        regs_dec<RADIAL_FWD_REGS_LO>();
     if (warp == 0) {
         // ------------------------------------------------------------ producer
         if (lane == 0) {
@@ -350,7 +351,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
     }
     } else {
-        regs_inc<RADIAL_REGS_HI>();
+        regs_inc<RADIAL_FWD_REGS_HI>();
         // ------------------------------------------------------------ softmax
         const int t = (warp - 4) >> 2;                 // Q tile
         const int r = ((warp & 3) << 5) + lane;        // row in tile = TMEM lane
