@@ -9,13 +9,13 @@
 // Deterministic, no atomics, three launches:
 //   bwd_prep    D and lse*log2(e) per query row, padded to whole 128-row blocks
 //               (+inf lse / 0 D beyond n, so padded rows contribute exactly 0)
-//   bwd_dq      one CTA per (head, query block I) over its CSR row: S, dP on
-//               tcgen05 into TMEM, dS (bf16) written back to TMEM, dQ += dS K (TS MMA)
-//   bwd_dkdv    one CTA per (head, KV block J) over its CSC column: S^T, dP^T,
-//               then dV += P^T dO and dK += dS^T Q with P^T / dS^T in TMEM
-// Both stream the other operand in 128-row blocks split into two 64-row
-// sub-steps whose S / dP TMEM buffers alternate, so the tensor core computes
-// sub-step s+1 while warpgroup (s mod 2) does the elementwise work of s.
+//   bwd_dq      one CTA per (head, query block I) over its CSR row: S = Q K^T (Q resident in
+//               TMEM), dP = dO V^T, dS (bf16) into its own TMEM columns, dQ += dS K
+//   bwd_dkdv    one CTA per (head, KV block J) over its CSC column: S^T, dP^T, then
+//               dV += P^T dO and dK += dS^T Q with P^T / dS^T in the consumed dP^T columns
+// Every MMA is 128 x 128 x 16 (128 x 64 MMAs run at 61% of the tensor rate); the elementwise
+// warpgroups split the 128 columns of each block and release S / dP as soon as they have
+// loaded them, so the tensor core computes the next block while they work.
 // Block size 128 only (the layouts of the BASELINE backward configs).
 #include <cmath>
 #include <cstdlib>
@@ -55,7 +55,6 @@ namespace {
 
 constexpr int kThreads = 384;   // warp0 TMA, warp1 MMA, warp2 TMEM alloc, warps 4-11 elementwise
 constexpr int kBlk = 128;       // layout block = rows per resident tile
-constexpr int kSub = 64;        // streamed rows per sub-step
 constexpr uint32_t kTmem = 0;   // whole-SM TMEM allocation starts at column 0
 constexpr float kLog2e = 1.4426950408889634f;
 
@@ -107,7 +106,6 @@ struct BwdCfg {
     static constexpr int kAtoms = D / 64;
     static constexpr int kAtomBytes = kBlk * 128;      // 128 rows x 128 B
     static constexpr int kTileBytes = kBlk * D * 2;    // one 128-row bf16 tile
-    static constexpr uint32_t kIdS = idesc_bf16(128, kSub, 0, 0);  // 128 x 64 x 16, K-major both
     static constexpr uint32_t kIdAcc = idesc_bf16(128, D, 0, 1);   // 128 x D x 16, B MN-major
     static constexpr uint32_t kIdAcc128 = idesc_bf16(128, kBlk, 0, 0);  // 128 x 128 x 16, K-major both
 };
@@ -121,16 +119,6 @@ __host__ __device__ constexpr uint32_t koff(int kk, int row0) {
     return static_cast<uint32_t>(((kk >> 2) * (kBlk * 128) + row0 * 128 + (kk & 3) * 32) >> 4);
 }
 __host__ __device__ constexpr uint32_t mnoff(int row0) { return static_cast<uint32_t>((row0 * 128) >> 4); }
-
-// K-major descriptor of MMA k-step kk (16 elements of d) for a 128-row tile,
-// optionally starting at row `row0` (multiple of 8).
-__device__ __forceinline__ uint64_t kdesc(uint32_t tile, int kk, int row0) {
-    return sdesc_sw128(tile + (kk >> 2) * (kBlk * 128) + row0 * 128 + (kk & 3) * 32, 16, 1024);
-}
-// MN-major descriptor (B operand with N = d) of 16 rows starting at `row0`.
-__device__ __forceinline__ uint64_t mndesc(uint32_t tile, int row0) {
-    return sdesc_sw128(tile + row0 * 128, kBlk * 128, 1024);
-}
 
 // ============================================================================ dQ
 // CTA per (head, query block I) over its CSR row.  Q is resident in TMEM (A operand of

@@ -386,18 +386,8 @@ __device__ __forceinline__ float ex2(float x) {
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
     return y;
 }
-// 2^x on the FMA pipe (Cody-Waite split + cubic on [-1/2, 1/2], max rel err 1.0e-4,
-// well under bf16's 3.9e-3): for x in [-125, 126].  Used for a share of the softmax
-// exponentials so MUFU.EX2 is not the only exp2 pipe.
-__device__ __forceinline__ float ex2_poly(float x) {
-    x = fmaxf(x, -125.0f);
-    const float magic = 12582912.0f;  // 1.5 * 2^23: x + magic rounds x to an integer
-    const float t = x + magic;
-    const float f = x - (t - magic);
-    const float q = fmaf(fmaf(fmaf(0.05500859f, f, 0.24221037f), f, 0.6932829f), f, 1.0f);
-    return __int_as_float(__float_as_int(q) + (__float_as_int(t) << 23));
-}
-// Packed-pair variant on the sm_100 f32x2 FMA path (FFMA2/FADD2: two lanes per issue).
+// 2^x on the FMA pipe for pairs (magic-number split + cubic on [-1/2, 1/2]); used for a
+// configurable share of the softmax exponentials (RADIAL_POLY_PAIRS, off: see DESIGN.md).
 __device__ __forceinline__ float2 ex2_poly2(float2 x) {
     // 2^x = 2^round(x) * p(f), f in [-1/2, 1/2]: magic-number rounding and a cubic on the FMA
     // pipe (f32x2), the exponent added with one LEA per element on the ALU pipe
