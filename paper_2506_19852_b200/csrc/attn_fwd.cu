@@ -80,6 +80,13 @@ constexpr int kBQ = 128;        // query rows per tile
 // is prefetched kSlots / 2 steps ahead (the L2 -> SM latency under load is ~1 step).
 constexpr int kSlots = 5;  // the MMA loop is unrolled by kSlots steps (constant slot indices)
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
+#ifndef RADIAL_P_PARTS
+#define RADIAL_P_PARTS 2
+#endif
+// P of a tile is published in kPParts key-column parts, each on its own barrier, so the
+// PV MMAs of the first parts run while the later parts' exponentials are computed
+// (measured at H33: 2 and 4 parts perform the same; 4 needs block size 128).
+constexpr int kPParts = RADIAL_P_PARTS;
 #ifndef RADIAL_POLY_PAIRS
 #define RADIAL_POLY_PAIRS 0  // measured on B200: MUFU-only is fastest with the current pipeline
 #endif
@@ -110,7 +117,7 @@ struct FwdCfg {
     static constexpr int kSmemQ = 0;
     static constexpr int kSmemKV = kSmemQ + 2 * kQBytes;          // unified K/V ring
     static constexpr int kSmemBar = kSmemKV + kSlots * kKVBytes;
-    static constexpr int kNumBars = 1 + 2 * kSlots + 2 + 4 + 2;
+    static constexpr int kNumBars = 1 + 2 * kSlots + 2 + 2 * kPParts + 2;
     static constexpr int kSmemBytes = kSmemBar + kNumBars * 8 + 16;
     static constexpr int kSmemAlloc = kSmemBytes + 1024;  // slack for 1024 B alignment
     // TMEM columns
@@ -134,8 +141,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint64_t* bar_full = bars + 1;
     uint64_t* bar_empty = bar_full + kSlots;
     uint64_t* bar_sfull = bar_empty + kSlots;  // [2]
-    uint64_t* bar_pready = bar_sfull + 2;          // [2 tiles][2 key halves]
-    uint64_t* bar_ofull = bar_pready + 4;          // [2]
+    uint64_t* bar_pready = bar_sfull + 2;          // [2 tiles][kPParts key parts]
+    uint64_t* bar_ofull = bar_pready + 2 * kPParts;  // [2]
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar_ofull + 2);
 
     const int warp = threadIdx.x >> 5;
@@ -171,8 +178,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         for (int t = 0; t < 2; ++t) {
             mbar_init(&bar_sfull[t], 1);
-            mbar_init(&bar_pready[2 * t], 4);  // one elected arrive per softmax warp
-            mbar_init(&bar_pready[2 * t + 1], 4);
+            for (int q = 0; q < kPParts; ++q) mbar_init(&bar_pready[kPParts * t + q], 4);  // one arrive per softmax warp
             mbar_init(&bar_ofull[t], 1);
         }
         fence_barrier_init();
@@ -269,21 +275,26 @@ __global__ void __launch_bounds__(kThreads, 1)
                     constexpr uint32_t p_col = T ? Cfg::kColS1 : Cfg::kColS0;
                     constexpr uint32_t o_col = T ? Cfg::kColO1 : Cfg::kColO0;
 
-                    static_for<2>([&](auto HC) {
+                    static_for<kPParts>([&](auto HC) {
                         constexpr int h = decltype(HC)::value;
-                        mbar_wait(&bar_pready[2 * T + h], pphase);
-                        TRACE(8 + 2 * T + h, j - 1);
+                        constexpr int KPP = BK / 16 / kPParts;  // K-steps (16 keys) per part
+                        mbar_wait(&bar_pready[kPParts * T + h], pphase);
+                        TRACE(8 + 2 * T + (h * 2) / kPParts, j - 1);
                         tc_fence_after();
 #if defined(RADIAL_FWD_WARP_MMA) && !defined(RADIAL_FWD_NO_GROUP)
-                        if constexpr (BK / 32 == 4) {
-                            // four K-steps per asm block (elected issue, no per-MMA overhead)
-                            constexpr int kk0 = h * 4;
-                            mma_ts_x4<((VSL * Cfg::kKVBytes + kk0 * 16 * 128) >> 4), 128>(
-                                kTmem + o_col, kTmem + p_col + kk0 * 8, dv, Cfg::kIdescO, (acc | kk0) ? 1u : 0u);
+                        if constexpr (KPP == 4 || KPP == 2) {
+                            // the part's K-steps in one asm block (elected issue)
+                            constexpr int kk0 = h * KPP;
+                            if constexpr (KPP == 4)
+                                mma_ts_x4<((VSL * Cfg::kKVBytes + kk0 * 16 * 128) >> 4), 128>(
+                                    kTmem + o_col, kTmem + p_col + kk0 * 8, dv, Cfg::kIdescO, (acc | kk0) ? 1u : 0u);
+                            else
+                                mma_ts_x2<((VSL * Cfg::kKVBytes + kk0 * 16 * 128) >> 4), 128>(
+                                    kTmem + o_col, kTmem + p_col + kk0 * 8, dv, Cfg::kIdescO, (acc | kk0) ? 1u : 0u);
                         } else
 #endif
-                        static_for<BK / 32>([&](auto KI) {
-                            constexpr int kk = h * (BK / 32) + decltype(KI)::value;
+                        static_for<KPP>([&](auto KI) {
+                            constexpr int kk = h * KPP + decltype(KI)::value;
                             FWD_MMA_TS<((VSL * Cfg::kKVBytes + kk * 16 * 128) >> 4)>(
                                 kTmem + o_col, kTmem + p_col + kk * 8, dv, Cfg::kIdescO, (acc | kk) ? 1u : 0u);
                         });
@@ -496,14 +507,15 @@ __global__ void __launch_bounds__(kThreads, 1)
             const float2 sl = make_float2(sl2, sl2), nm = make_float2(-mb, -mb);
             auto half = [&](int h, auto POLY) {
                 constexpr int NP = decltype(POLY)::value;
-                uint32_t pk[BK / 4];
+                constexpr int CP = BK / kPParts;  // columns per part
+                static_assert(CP >= 32 && CP % 32 == 0, "P parts must be whole 32-column groups");
+                uint32_t pk[CP / 2];
 #pragma unroll
-                for (int c = h * (BK / 2); c < (h + 1) * (BK / 2); c += 2) {
+                for (int c = h * CP; c < (h + 1) * CP; c += 2) {
                     // store each 32-column group of P as soon as it is packed, so its
                     // tcgen05.st latency overlaps the next group's exponentials
-                    if (c > h * (BK / 2) && (c - h * (BK / 2)) % 32 == 0)
-                        tmem_st16(s_addr + h * (BK / 4) + (c - h * (BK / 2)) / 2 - 16,
-                                  pk + (c - h * (BK / 2)) / 2 - 16);
+                    if (c > h * CP && (c - h * CP) % 32 == 0)
+                        tmem_st16(s_addr + h * (CP / 2) + (c - h * CP) / 2 - 16, pk + (c - h * CP) / 2 - 16);
                     const float2 x = __ffma2_rn(make_float2(s[c], s[c + 1]), sl, nm);
                     float2 pr;
                     if (((c >> 1) & 7) < NP) {
@@ -516,17 +528,17 @@ __global__ void __launch_bounds__(kThreads, 1)
                         r2b = __fadd2_rn(r2b, pr);
                     else
                         r2a = __fadd2_rn(r2a, pr);
-                    pk[(c - h * (BK / 2)) / 2] = pack_bf16(pr.x, pr.y);
+                    pk[(c - h * CP) / 2] = pack_bf16(pr.x, pr.y);
                 }
-                tmem_st16(s_addr + h * (BK / 4) + BK / 4 - 16, pk + BK / 4 - 16);
+                tmem_st16(s_addr + h * (CP / 2) + CP / 2 - 16, pk + CP / 2 - 16);
                 tmem_wait_st();
                 tc_fence_before();
                 __syncwarp();
-                if (lane == 0) mbar_arrive(&bar_pready[2 * t + h]);
-                if ((warp & 3) == 0 && lane == 0) TRACE(4 * t + 2 + h, j);
+                if (lane == 0) mbar_arrive(&bar_pready[kPParts * t + h]);
+                if ((warp & 3) == 0 && lane == 0) TRACE(4 * t + 2 + (h * 2) / kPParts, j);
             };
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
+            for (int h = 0; h < kPParts; ++h) {
                 if (kPolyPairs > 0 && full)
                     half(h, std::integral_constant<int, kPolyPairs>{});
                 else
