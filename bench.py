@@ -237,12 +237,20 @@ def run_ours(args, world, rank, local):
     lse = torch.empty(Hl, n, device=dev, dtype=torch.float32)
 
     o_full = None
-    if args.gather and world > 1:
+    fused = None
+    if args.gather and world > 1 and not args.gather_nccl:
+        # C1 fused into the kernel: O rows stored straight into every rank's full buffer
+        fused = _HP.full_output(H, n, d)
+    elif args.gather and world > 1:
         o_full = torch.empty(H, n, d, device=dev, dtype=torch.bfloat16)
 
     def step():
+        if fused is not None:
+            P.masked_attention_scatter(q, k, v, lay, fused.ptrs, fused.head_base, H, lse=lse, stream=stream)
+            fused.sync()
+            return
         P.masked_attention(q, k, v, lay, out=o, lse=lse, return_lse=True, stream=stream)
-        if o_full is not None:  # C1: reassemble O [H, n, d] on every rank over NVLink
+        if o_full is not None:  # C1: reassemble O [H, n, d] on every rank (NCCL all-gather)
             _HP.gather_heads(o, H, out=o_full)
 
     for _ in range(args.warmup):
@@ -344,7 +352,9 @@ def run_ours(args, world, rank, local):
                                f"head_dim {d}, block {B}, sink on; heads split {Hl}/rank",
                    "frames": f, "tokens_per_frame": s, "heads": H, "head_dim": d, "block": B,
                    "kept_blocks": kept, "block_sparsity": 1 - kept / float(lay.grid_rows ** 2),
-                   "parallelism": f"head-parallel x{world}" + (" + all-gather(O)" if args.gather and world > 1 else ""),
+                   "parallelism": f"head-parallel x{world}" + ((" + NCCL all-gather(O)" if args.gather_nccl else
+                                                                 " + O stored to every rank from the epilogue")
+                                                                if args.gather and world > 1 else ""),
                    "l2": "inputs (3 x bf16 [H][n][d]) far exceed the 126 MB L2; no flush"},
         "kernel_ms": kernel_ms,
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
@@ -404,7 +414,10 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--bwd", action="store_true", help="also time the backward (K3)")
     ap.add_argument("--gather", action="store_true",
-                    help="include the NCCL all-gather of O (C1) in each step when N > 1")
+                    help="reassemble O [H, n, d] on every rank in each step when N > 1 (C1): the kernel "
+                         "epilogue stores each row into every rank's buffer over peer memory")
+    ap.add_argument("--gather-nccl", action="store_true",
+                    help="with --gather: NCCL all-gather after the kernel instead (comparison)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -104,6 +104,18 @@ int radial_cuda_attn_fwd(const void* q, const void* k, const void* v, void* o, f
                          uint32_t heads, uint64_t n, uint32_t head_dim, float scale,
                          const radial_layout* layout, void* stream);
 
+/* ---- fused head-parallel reassembly (SURVEY 8e, C1 without a separate all-gather):
+ *      the forward of radial_cuda_attn_fwd for this rank's `heads` heads, with every O row
+ *      stored directly into each of the n_dst (1..8) destination buffers bf16
+ *      [heads_full][n][head_dim] at head head_base + h -- typically every rank's full-O
+ *      buffer mapped as peer memory (NVLink / NVSwitch P2P stores issued from the kernel
+ *      epilogue while other CTAs still compute).  The caller synchronises the ranks
+ *      afterwards (e.g. a symmetric-memory barrier).  lse (this call's heads) may be NULL. */
+int radial_cuda_attn_fwd_scatter(const void* q, const void* k, const void* v, void* const* o_dst,
+                                 uint32_t n_dst, uint32_t head_base, uint32_t heads_full, float* lse,
+                                 uint32_t heads, uint64_t n, uint32_t head_dim, float scale,
+                                 const radial_layout* layout, void* stream);
+
 /* ---- token-exact forward: replaces radial::masked_attention(const AttentionInstance&,
  *      const PatternSpec&) (attention.hpp:184-225).  Iterates the blocks of a layout built
  *      by radial_cuda_mask_build (a superset, block.hpp:59) and keeps exactly the token

@@ -89,6 +89,8 @@ _sig("radial_cuda_layout_device_csr", _i32, _vp, C.POINTER(_vp), C.POINTER(_vp))
 _sig("radial_cuda_layout_free", None, _vp)
 _sig("radial_cuda_attn_fwd", _i32, _vp, _vp, _vp, _vp, _vp, _u32, _u64, _u32, _f32, _vp, _vp)
 _sig("radial_cuda_attn_fwd_token", _i32, _vp, _vp, _vp, _vp, _vp, _u32, _u64, _u32, _f32, _vp, _vp)
+_sig("radial_cuda_attn_fwd_scatter", _i32, _vp, _vp, _vp, C.POINTER(_vp), _u32, _u32, _u32, _vp, _u32, _u64,
+     _u32, _f32, _vp, _vp)
 _sig("radial_cuda_attn_fwd_dense", _i32, _vp, _vp, _vp, _vp, _vp, _u32, _u64, _u32, _u32, _f32, _vp)
 _sig("radial_cuda_attn_fwd_host", _i32, _vp, _vp, _vp, _vp, _vp, _u32, _u64, _u32, _f32, _vp, _vp)
 _sig("radial_cuda_attn_bwd_workspace_size", C.c_size_t, _u32, _u64, _u32)
@@ -487,6 +489,23 @@ def masked_attention(q, k, v, layout, scale: Optional[float] = None, *, out=None
                                      lse.data_ptr() if lse is not None else None, H, n, d,
                                      float(scale or 0.0), L.handle, _stream_ptr(stream)))
     return (o, lse) if return_lse else o
+
+
+def masked_attention_scatter(q, k, v, layout, dst_ptrs, head_base: int, heads_full: int,
+                             scale: Optional[float] = None, *, lse=None, stream=None):
+    """Head-parallel forward with the reassembly fused into the kernel epilogue: every O
+    row of these heads is stored into each buffer of `dst_ptrs` (1..8 device pointers to bf16
+    [heads_full, n, head_dim], e.g. every rank's full-O buffer mapped as peer memory) at
+    head `head_base + h`.  The caller synchronises the ranks afterwards."""
+    H, n, d = _check_qkv(q, k, v)
+    L = _as_device_layout(layout)
+    if L.shape.total_tokens() != n:
+        raise ValueError("masked_attention: layout shape mismatch")
+    ptrs = (_vp * len(dst_ptrs))(*[int(x) for x in dst_ptrs])
+    _check(_lib.radial_cuda_attn_fwd_scatter(q.data_ptr(), k.data_ptr(), v.data_ptr(), ptrs, len(dst_ptrs),
+                                             head_base, heads_full,
+                                             lse.data_ptr() if lse is not None else None, H, n, d,
+                                             float(scale or 0.0), L.handle, _stream_ptr(stream)))
 
 
 def masked_attention_pattern(q, k, v, shape: GridShape, pattern: PatternSpec, scale: Optional[float] = None,

@@ -92,9 +92,16 @@ constexpr int kPParts = RADIAL_P_PARTS;
 #endif
 constexpr int kPolyPairs = RADIAL_POLY_PAIRS;  // column pairs per 8 using the polynomial exp2
 
+constexpr int kMaxDst = 8;  // fused all-gather: O rows stored into up to 8 ranks' buffers
+
 struct FwdParams {
     __nv_bfloat16* o;
     float* lse;
+    // fused reassembly (C1 without a separate collective): when n_dst > 0 each O row is
+    // stored into every destination [heads_full][n][D] buffer (peer GPUs' memory over
+    // NVLink / NVSwitch) at head head_base + head, instead of into o
+    __nv_bfloat16* dst[kMaxDst];
+    uint32_t n_dst, head_base, heads_full;
     const uint64_t* uptr;
     const uint32_t* uidx;
     const uint32_t* order;
@@ -551,6 +558,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_after();
         const float inv = l > 0.f ? 1.f / l : 0.f;
         __nv_bfloat16* orow = p.o + (static_cast<uint64_t>(head) * p.n + grow) * D;
+        const uint64_t frow = (static_cast<uint64_t>(p.head_base + head) * p.n + grow) * D;
 #pragma unroll
         for (int c = 0; c < D; c += 32) {
             uint32_t u[32];
@@ -561,9 +569,20 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int x = 0; x < 16; ++x)
                 w[x] = pack_bf16(__uint_as_float(u[2 * x]) * inv, __uint_as_float(u[2 * x + 1]) * inv);
             if (grow < p.n) {
-                uint4* dst = reinterpret_cast<uint4*>(orow + c);
+                if (p.n_dst == 0) {
+                    uint4* dst = reinterpret_cast<uint4*>(orow + c);
 #pragma unroll
-                for (int x = 0; x < 4; ++x) dst[x] = make_uint4(w[4 * x], w[4 * x + 1], w[4 * x + 2], w[4 * x + 3]);
+                    for (int x = 0; x < 4; ++x) dst[x] = make_uint4(w[4 * x], w[4 * x + 1], w[4 * x + 2], w[4 * x + 3]);
+                } else {
+                    // every rank's full O: stores to peer GPUs go straight over NVLink while the
+                    // other CTAs are still computing (no all-gather after the kernel)
+                    for (uint32_t r = 0; r < p.n_dst; ++r) {
+                        uint4* dst = reinterpret_cast<uint4*>(p.dst[r] + frow + c);
+#pragma unroll
+                        for (int x = 0; x < 4; ++x)
+                            dst[x] = make_uint4(w[4 * x], w[4 * x + 1], w[4 * x + 2], w[4 * x + 3]);
+                    }
+                }
             }
         }
         if (p.lse && grow < p.n)
@@ -621,7 +640,7 @@ int make_tmap_bf16_3d(CUtensorMap* m, const void* base, uint64_t n, uint32_t D, 
 template <int D, int BK>
 int launch_fwd_t(const void* q, const void* k, const void* v, void* o, float* lse,
                  uint32_t heads, uint64_t n, float scale, const radial_layout* L, uint32_t R,
-                 bool token, cudaStream_t st) {
+                 bool token, cudaStream_t st, const FwdScatter* sc) {
     using Cfg = FwdCfg<D, BK>;
     CUtensorMap tq, tk, tv;
     int rc;
@@ -631,6 +650,12 @@ int launch_fwd_t(const void* q, const void* k, const void* v, void* o, float* ls
     FwdParams p{};
     p.o = static_cast<__nv_bfloat16*>(o);
     p.lse = lse;
+    if (sc) {
+        p.n_dst = sc->n_dst;
+        p.head_base = sc->head_base;
+        p.heads_full = sc->heads_full;
+        for (uint32_t r = 0; r < sc->n_dst; ++r) p.dst[r] = static_cast<__nv_bfloat16*>(sc->dst[r]);
+    }
     p.n = n;
     p.heads = heads;
     p.R = R;
@@ -666,14 +691,16 @@ extern "C" int radial_cuda_debug_trace(void* buf) {
 
 int launch_fwd(const void* q, const void* k, const void* v, void* o, float* lse, uint32_t heads,
                uint64_t n, uint32_t D, uint32_t BK, float scale, const radial_layout* L,
-               cudaStream_t st, bool token) {
+               cudaStream_t st, bool token, const FwdScatter* sc) {
     const uint64_t R64 = (n + BK - 1) / BK;
     if (R64 >= (1ull << 28)) return fail(RADIAL_ERR_INVALID, "block grid too large for the kernel");
     const uint32_t R = static_cast<uint32_t>(R64);
-    if (D == 128 && BK == 128) return launch_fwd_t<128, 128>(q, k, v, o, lse, heads, n, scale, L, R, token, st);
-    if (D == 128 && BK == 64) return launch_fwd_t<128, 64>(q, k, v, o, lse, heads, n, scale, L, R, token, st);
-    if (D == 64 && BK == 128) return launch_fwd_t<64, 128>(q, k, v, o, lse, heads, n, scale, L, R, token, st);
-    if (D == 64 && BK == 64) return launch_fwd_t<64, 64>(q, k, v, o, lse, heads, n, scale, L, R, token, st);
+    if (sc && (sc->n_dst < 1 || sc->n_dst > static_cast<uint32_t>(kMaxDst)))
+        return fail(RADIAL_ERR_INVALID, "attn_fwd_scatter: 1..8 destination buffers");
+    if (D == 128 && BK == 128) return launch_fwd_t<128, 128>(q, k, v, o, lse, heads, n, scale, L, R, token, st, sc);
+    if (D == 128 && BK == 64) return launch_fwd_t<128, 64>(q, k, v, o, lse, heads, n, scale, L, R, token, st, sc);
+    if (D == 64 && BK == 128) return launch_fwd_t<64, 128>(q, k, v, o, lse, heads, n, scale, L, R, token, st, sc);
+    if (D == 64 && BK == 64) return launch_fwd_t<64, 64>(q, k, v, o, lse, heads, n, scale, L, R, token, st, sc);
     return fail(RADIAL_ERR_INVALID, "masked_attention: head_dim must be 64 or 128 and block_size 64 or 128");
 }
 

@@ -25,7 +25,7 @@ int cuda_fail(cudaError_t e, const char* where) {
 
 int launch_fwd(const void* q, const void* k, const void* v, void* o, float* lse, uint32_t heads,
                uint64_t n, uint32_t D, uint32_t BK, float scale, const radial_layout* L,
-               cudaStream_t st, bool token = false);
+               cudaStream_t st, bool token = false, const FwdScatter* sc = nullptr);
 int launch_bwd(const void* q, const void* k, const void* v, const void* o, const float* lse,
                const void* dout, void* dq, void* dk, void* dv, uint32_t heads, uint64_t n,
                uint32_t D, float scale, const radial_layout* L, void* workspace, cudaStream_t st);
@@ -358,6 +358,28 @@ int radial_cuda_attn_fwd(const void* q, const void* k, const void* v, void* o, f
     if ((rc = check_layout_for_attn(layout, n))) return rc;
     return launch_fwd(q, k, v, o, lse, heads, n, head_dim, layout->B, resolve_scale(scale, head_dim), layout,
                       static_cast<cudaStream_t>(stream));
+}
+
+int radial_cuda_attn_fwd_scatter(const void* q, const void* k, const void* v, void* const* o_dst,
+                                 uint32_t n_dst, uint32_t head_base, uint32_t heads_full, float* lse,
+                                 uint32_t heads, uint64_t n, uint32_t head_dim, float scale,
+                                 const radial_layout* layout, void* stream) {
+    if (!o_dst || n_dst < 1 || n_dst > 8)
+        return fail(RADIAL_ERR_INVALID, "attn_fwd_scatter: 1..8 destination buffers");
+    for (uint32_t r = 0; r < n_dst; ++r)
+        if (!o_dst[r]) return fail(RADIAL_ERR_INVALID, "attn_fwd_scatter: null destination buffer");
+    if (static_cast<uint64_t>(head_base) + heads > heads_full)
+        return fail(RADIAL_ERR_INVALID, "attn_fwd_scatter: head_base + heads exceeds heads_full");
+    int rc = check_attn(q, k, v, o_dst[0], heads, n, head_dim);
+    if (rc) return rc;
+    if ((rc = check_layout_for_attn(layout, n))) return rc;
+    FwdScatter sc{};
+    for (uint32_t r = 0; r < n_dst; ++r) sc.dst[r] = o_dst[r];
+    sc.n_dst = n_dst;
+    sc.head_base = head_base;
+    sc.heads_full = heads_full;
+    return launch_fwd(q, k, v, o_dst[0], lse, heads, n, head_dim, layout->B, resolve_scale(scale, head_dim),
+                      layout, static_cast<cudaStream_t>(stream), false, &sc);
 }
 
 int radial_cuda_attn_fwd_token(const void* q, const void* k, const void* v, void* o, float* lse,

@@ -44,6 +44,13 @@ struct radial_layout {
 
 namespace radial_detail {
 
+// Fused reassembly of O across ranks (radial_cuda_attn_fwd_scatter): destination buffers
+// [heads_full][n][D] (one per rank, peer pointers), this call's heads at head_base.
+struct FwdScatter {
+    void* dst[8];
+    uint32_t n_dst, head_base, heads_full;
+};
+
 void set_error(const std::string& msg);
 int fail(int code, const std::string& msg);
 int cuda_fail(cudaError_t e, const char* where);

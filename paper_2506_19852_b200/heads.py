@@ -87,6 +87,13 @@ class HeadParallel:
         trimmed = [p[:sz] for p, sz in zip(parts, sizes)]
         return torch.cat(trimmed, 0) if out is None else torch.cat(trimmed, 0, out=out)
 
+    def full_output(self, total_heads: int, n: int, d: int, force_symmetric: bool = False):
+        """FusedOutput: a [total_heads, n, d] bf16 buffer on every rank, mapped into every
+        other rank's address space (torch symmetric memory over NVLink / NVSwitch), for
+        masked_attention_scatter: each rank's kernel epilogue stores its heads' O rows into
+        all ranks' buffers, so no all-gather runs after the kernel."""
+        return FusedOutput(self, total_heads, n, d, force_symmetric)
+
     def heads_of(self, rank: int, total: int) -> int:
         lo, hi = head_slice(total, self.world, rank)
         return hi - lo
@@ -95,3 +102,33 @@ class HeadParallel:
         if self.world > 1:
             import torch.distributed as dist
             dist.destroy_process_group()
+
+
+class FusedOutput:
+    """Full-O buffer shared across ranks for the fused reassembly (C1 without a collective).
+
+    `ptrs` lists every rank's buffer as a device pointer valid on this rank (peer memory);
+    `head_base` is this rank's first head.  After the forward, `sync()` makes all ranks'
+    stores visible (symmetric-memory barrier).  World size 1 degenerates to a local buffer."""
+
+    def __init__(self, hp: HeadParallel, total_heads: int, n: int, d: int, force_symmetric: bool = False):
+        import torch
+        self.hp = hp
+        self.head_base, hi = hp.heads(total_heads)
+        self.heads_full = total_heads
+        dev = torch.device("cuda", torch.cuda.current_device())
+        if hp.world > 1 or force_symmetric:
+            import torch.distributed as dist
+            import torch.distributed._symmetric_memory as symm_mem
+            self.out = symm_mem.empty(total_heads, n, d, dtype=torch.bfloat16, device=dev)
+            self._hdl = symm_mem.rendezvous(self.out, dist.group.WORLD)
+            self.ptrs = [int(p) for p in self._hdl.buffer_ptrs]
+        else:
+            self.out = torch.empty(total_heads, n, d, dtype=torch.bfloat16, device=dev)
+            self._hdl = None
+            self.ptrs = [self.out.data_ptr()]
+
+    def sync(self):
+        """All ranks' epilogue stores have landed in every buffer once this returns."""
+        if self._hdl is not None:
+            self._hdl.barrier()

@@ -97,3 +97,23 @@ def test_grid_shape_and_pattern_validation():
         P.GridShape(1 << 20, 1 << 13)
     with pytest.raises(ValueError, match="temporal_window"):
         P.PatternSpec(P.PatternKind.sta, False, None, 2).validate()
+
+
+def test_scatter_forward_argument_validation():
+    """radial_cuda_attn_fwd_scatter rejects bad destination lists before touching the GPU."""
+    import paper_2506_19852_b200 as P
+    lib = P._lib
+    VP = ctypes.c_void_p
+    fake = VP(0x1000)
+    dst = (VP * 9)(*([0x2000] * 9))
+    lib.radial_cuda_last_error.restype = ctypes.c_char_p
+
+    def call(n_dst, head_base, heads_full, heads=2, ptrs=dst):
+        return lib.radial_cuda_attn_fwd_scatter(fake, fake, fake, ptrs, n_dst, head_base, heads_full, None,
+                                               heads, 4096, 128, ctypes.c_float(0.0), None, None)
+    assert call(0, 0, 2) == 1 and b"destination" in lib.radial_cuda_last_error()
+    assert call(9, 0, 2) == 1
+    assert call(2, 7, 8) == 1 and b"heads_full" in lib.radial_cuda_last_error()
+    nulls = (VP * 2)(0x2000, 0)
+    assert call(2, 0, 2, ptrs=nulls) == 1 and b"null destination" in lib.radial_cuda_last_error()
+    assert call(1, 0, 2) == 1 and b"null layout" in lib.radial_cuda_last_error()

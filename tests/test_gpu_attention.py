@@ -1,5 +1,7 @@
 """GPU parity: K2 sparse forward and K4 dense forward against the fp64 oracle (and the
 reference itself where it is cheap), per (head, query block)."""
+import os
+
 import numpy as np
 import pytest
 
@@ -8,6 +10,7 @@ from tests._util import (assert_within, bf16_bits, bits_to_f32, block_errors, in
                          to_torch_bf16)
 
 pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 @pytest.fixture(scope="module")
@@ -181,6 +184,44 @@ def test_paper_scale_hunyuan33_sampled_blocks(P):
         want = O.attention_rows(qh, kh, vh, B, host.row_ptr, host.col_idx, rows)
         got = o[h].float().cpu().numpy()[rows]
         assert_within(block_errors(got, want, rows, B), f"H33 head {h}")
+
+
+def test_scatter_epilogue_writes_every_destination(P):
+    """masked_attention_scatter (fused C1 reassembly): O rows of these heads land in every
+    destination buffer at head_base + h, bit-identical to masked_attention, and nothing
+    else in the buffers is touched (two local buffers stand in for two ranks' memory)."""
+    import torch
+    f, s, B, d, H, Hfull, base = 5, 300, 128, 128, 3, 8, 4
+    n = f * s
+    g = torch.Generator(device="cuda").manual_seed(3)
+    q, k, v = (torch.randn(H, n, d, device="cuda", generator=g).to(torch.bfloat16) for _ in range(3))
+    lay = P.device_layout(P.GridShape(f, s), P.PatternSpec.radial(), B)
+    o_ref, lse_ref = P.masked_attention(q, k, v, lay, return_lse=True)
+    sentinel = torch.tensor(7.25, dtype=torch.bfloat16)
+    bufs = [torch.full((Hfull, n, d), 7.25, dtype=torch.bfloat16, device="cuda") for _ in range(2)]
+    lse = torch.empty(H, n, device="cuda")
+    P.masked_attention_scatter(q, k, v, lay, [b.data_ptr() for b in bufs], base, Hfull, lse=lse)
+    torch.cuda.synchronize()
+    for b in bufs:
+        assert torch.equal(b[base:base + H], o_ref)
+        assert bool((b[:base] == sentinel).all()) and bool((b[base + H:] == sentinel).all())
+    assert torch.equal(lse, lse_ref)
+
+
+def test_fused_reassembly_through_symmetric_memory():
+    """The multi-rank plumbing of the fused reassembly (torch symmetric memory rendezvous,
+    peer pointers, barrier) under torchrun with the ranks this box has (1 here): every
+    rank's full-O buffer equals the single-GPU forward of all heads."""
+    import subprocess
+    import sys
+    import torch
+    nproc = max(1, min(torch.cuda.device_count(), 8))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
+           "--master-addr", "127.0.0.1", "--master-port", "29561",
+           os.path.join(ROOT, "scripts", "fused_gather_check.py")]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=240)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-4000:]
+    assert '"identical": true' in r.stdout
 
 
 @pytest.mark.parametrize("f,s,H", [(21, 3600, 40), (28, 1590, 24), (132, 3600, 24)],
