@@ -381,6 +381,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         // token coordinates (frame, position) of this row, for the token-exact mode
         const uint32_t tok_i = TOKEN ? static_cast<uint32_t>(grow / p.rule.s) : 0u;
         const uint32_t tok_k = TOKEN ? static_cast<uint32_t>(grow % p.rule.s) : 0u;
+        uint32_t tok_jf = 0, tok_fs = 0;  // token mode: key frame (and its first key) of the current block
         const float sl2 = p.scale_log2;
         float m = -INFINITY, l = 0.f;
         uint32_t sphase = 0;
@@ -435,11 +436,22 @@ __global__ void __launch_bounds__(kThreads, 1)
                 for (int w = 0; w < BK / 32; ++w) kmask[w] = 0u;
                 if (active && grow < p.n) {
                     const uint32_t v0 = J * BK, v1 = v0 + static_cast<uint32_t>(valid) - 1;
-                    for (uint32_t jf = v0 / p.rule.s; jf * p.rule.s <= v1; ++jf) {
+                    // key frame of the block's first key, tracked incrementally (the KV list is
+                    // ascending) instead of a division per block
+                    if (v0 < tok_fs) {
+                        tok_jf = v0 / p.rule.s;
+                        tok_fs = tok_jf * p.rule.s;
+                    }
+                    while (tok_fs + p.rule.s <= v0) {
+                        ++tok_jf;
+                        tok_fs += p.rule.s;
+                    }
+                    uint32_t fs = tok_fs;
+                    for (uint32_t jf = tok_jf; fs <= v1; ++jf, fs += p.rule.s) {
                         uint32_t lo, hi;
                         if (!radial_rule::kept_span(p.rule, tok_i, tok_k, tok_k, jf, lo, hi)) continue;
-                        const uint32_t a = max(jf * p.rule.s + lo, v0) - v0;
-                        const uint32_t b = min(jf * p.rule.s + hi, v1);
+                        const uint32_t a = max(fs + lo, v0) - v0;
+                        const uint32_t b = min(fs + hi, v1);
                         if (b < v0 || a > b - v0) continue;
                         const uint32_t bb = b - v0;
 #pragma unroll
@@ -456,6 +468,10 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                 for (int w = 0; w < BK / 32; ++w) all = all && kmask[w] == 0xffffffffu;
                 full = active && all;
+#ifdef RADIAL_TOK_EXP  // timing experiment: 1 = kmask built but never applied (wrong results)
+                if (kmask[0] == 0x12345u && kmask[1] == 7u) s[0] = 0.f;  // keep the build alive
+                full = active && valid == BK;
+#endif
             }
             if (!full) {
                 // rare (tail KV block, a row whose query block skips J, or a token-masked
