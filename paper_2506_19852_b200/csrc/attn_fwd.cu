@@ -468,10 +468,6 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                 for (int w = 0; w < BK / 32; ++w) all = all && kmask[w] == 0xffffffffu;
                 full = active && all;
-#ifdef RADIAL_TOK_EXP  // timing experiment: 1 = kmask built but never applied (wrong results)
-                if (kmask[0] == 0x12345u && kmask[1] == 7u) s[0] = 0.f;  // keep the build alive
-                full = active && valid == BK;
-#endif
             }
             if (!full) {
                 // rare (tail KV block, a row whose query block skips J, or a token-masked
