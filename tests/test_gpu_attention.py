@@ -92,6 +92,29 @@ def test_ragged_shapes_vs_oracle(P, f, s, B, d, sink):
         assert np.abs(lse[h] - wl).max() < 2e-2
 
 
+def test_random_shape_fuzz_vs_oracle(P):
+    """40 random grids (frames 1-20, tokens per frame 1-700, block 64/128, head_dim 64/128,
+    sink on/off, 1-3 heads): every query block of every head against the fp64 oracle --
+    exercises short KV lists (fewer steps than the K/V ring), tails inside a tile, and
+    chunks whose second tile is past the grid."""
+    rng = np.random.default_rng(2025)
+    for case in range(40):
+        f = int(rng.integers(1, 21))
+        s = int(rng.integers(1, 701))
+        if f * s < 2:
+            continue
+        B = int(rng.choice([64, 128]))
+        d = int(rng.choice([64, 128]))
+        sink = bool(rng.integers(0, 2))
+        H = int(rng.integers(1, 4))
+        q, k, v, host, o, lse = _run_sparse(P, f, s, B, d, H, sink=sink, seed0=100 + case)
+        rows = np.arange(f * s)
+        for h in range(H):
+            want, wl = O.attention_rows(q[h], k[h], v[h], B, host.row_ptr, host.col_idx, rows, want_lse=True)
+            assert_within(block_errors(o[h], want, rows, B), f"case {case}: f{f}s{s}B{B}d{d}sink{sink} head {h}")
+            assert np.abs(lse[h] - wl).max() < 2e-2, f"case {case} lse"
+
+
 @pytest.mark.parametrize("B,d", [(128, 128), (64, 64)])
 def test_peaked_logits_q_times_8(P, B, d):
     f, s, H = 6, 400, 2
