@@ -320,6 +320,42 @@ def test_token_exact_forward_vs_oracle(P, f, s, B, d, kind, sink, tw, sw):
         assert np.abs(lse[h].cpu().numpy() - wl).max() < 2e-2 if hasattr(lse, "cpu") else True
 
 
+def test_token_exact_random_fuzz_vs_oracle(P):
+    """24 random token-exact cases over every frame-structured kind (radial, dense, spatial,
+    temporal, sta, harmonic) with random windows, sink, block and head_dim."""
+    import torch
+    rng = np.random.default_rng(4242)
+    kinds = ["radial", "dense", "spatial", "temporal", "sta", "harmonic"]
+    for case in range(24):
+        kind = kinds[case % len(kinds)]
+        f = int(rng.integers(1, 14))
+        s = int(rng.integers(2, 401))
+        B = int(rng.choice([64, 128]))
+        d = int(rng.choice([64, 128]))
+        sink = bool(rng.integers(0, 2))
+        tw = int(rng.integers(0, 4))
+        sw = int(rng.integers(0, s))
+        spec = {"radial": lambda: P.PatternSpec.radial(sink), "dense": lambda: P.PatternSpec.dense(),
+                "spatial": lambda: P.PatternSpec.spatial(tw, sink),
+                "temporal": lambda: P.PatternSpec.temporal(sw, sink),
+                "sta": lambda: P.PatternSpec.sta(tw, sw, sink),
+                "harmonic": lambda: P.PatternSpec.harmonic(sink)}[kind]()
+        q, k, v = instance_bf16(f, s, d, 1, 500 + case)
+        try:
+            o = P.masked_attention_pattern(to_torch_bf16(q), to_torch_bf16(k), to_torch_bf16(v), P.GridShape(f, s),
+                                           spec, block_size=B)
+        except RuntimeError as e:  # a row that keeps no key: the reference throws too
+            assert "keeps no keys" in str(e), e
+            continue
+        torch.cuda.synchronize()
+        rows = np.arange(f * s)
+        want = O.token_attention_rows(q[0], k[0], v[0], f, s, rows,
+                                      "dense" if kind == "dense" else kind,
+                                      True if kind == "dense" else sink, tw, sw)
+        assert_within(block_errors(o[0].float().cpu().numpy(), want, rows, B),
+                      f"case {case}: {kind} f{f}s{s}B{B}d{d}sink{sink}tw{tw}sw{sw}")
+
+
 @pytest.mark.skipif(not O.ref_available(), reason="oracle/_ref not built")
 def test_token_exact_forward_vs_reference_library(P):
     import torch
