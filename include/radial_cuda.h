@@ -144,6 +144,17 @@ int radial_cuda_attn_fwd_host(const void* q, const void* k, const void* v, void*
                               uint32_t heads, uint64_t n, uint32_t head_dim, float scale,
                               const radial_layout* layout, void* stream);
 
+/* ---- head-parallel host-buffer forward over several GPUs of this node:
+ *      builds the pattern's block layout (radial_cuda_mask_build) on each listed device
+ *      and runs radial_cuda_attn_fwd_host on an even split of the heads there, one host
+ *      thread per device -- the multi-GPU path for C / C++ callers without torchrun.
+ *      Host buffers as for radial_cuda_attn_fwd_host (pinned for overlap); synchronous. */
+int radial_cuda_attn_fwd_host_multi(const void* q, const void* k, const void* v, void* o, float* lse,
+                                    uint32_t heads, uint64_t n, uint32_t head_dim, float scale,
+                                    uint32_t frames, uint32_t tokens_per_frame, uint32_t block_size, int kind,
+                                    int sink, uint32_t temporal_window, uint32_t spatial_window,
+                                    const int* devices, int num_devices);
+
 /* ---- host-buffer dense comparator (dense_attention's call shape, attention.hpp:141). */
 int radial_cuda_attn_fwd_dense_host(const void* q, const void* k, const void* v, void* o, float* lse,
                                     uint32_t heads, uint64_t n, uint32_t head_dim, uint32_t block_size,

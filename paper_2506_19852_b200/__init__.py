@@ -89,6 +89,8 @@ _sig("radial_cuda_layout_device_csr", _i32, _vp, C.POINTER(_vp), C.POINTER(_vp))
 _sig("radial_cuda_layout_free", None, _vp)
 _sig("radial_cuda_attn_fwd", _i32, _vp, _vp, _vp, _vp, _vp, _u32, _u64, _u32, _f32, _vp, _vp)
 _sig("radial_cuda_attn_fwd_token", _i32, _vp, _vp, _vp, _vp, _vp, _u32, _u64, _u32, _f32, _vp, _vp)
+_sig("radial_cuda_attn_fwd_host_multi", _i32, _vp, _vp, _vp, _vp, _vp, _u32, _u64, _u32, _f32, _u32, _u32, _u32,
+     _i32, _i32, _u32, _u32, C.POINTER(_i32), _i32)
 _sig("radial_cuda_attn_fwd_scatter", _i32, _vp, _vp, _vp, C.POINTER(_vp), _u32, _u32, _u32, _vp, _u32, _u64,
      _u32, _f32, _vp, _vp)
 _sig("radial_cuda_attn_fwd_dense", _i32, _vp, _vp, _vp, _vp, _vp, _u32, _u64, _u32, _u32, _f32, _vp)

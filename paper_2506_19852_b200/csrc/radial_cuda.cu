@@ -4,6 +4,8 @@
 #include <new>
 #include <mutex>
 #include <string>
+#include <thread>
+#include <algorithm>
 #include <vector>
 
 #include "radial_internal.h"
@@ -415,6 +417,57 @@ int radial_cuda_attn_fwd_host(const void* q, const void* k, const void* v, void*
     if ((rc = check_layout_for_attn(layout, n))) return rc;
     return host_fwd(q, k, v, o, lse, heads, n, head_dim, layout->B, scale, layout,
                     static_cast<cudaStream_t>(stream));
+}
+
+int radial_cuda_attn_fwd_host_multi(const void* q, const void* k, const void* v, void* o, float* lse,
+                                    uint32_t heads, uint64_t n, uint32_t head_dim, float scale,
+                                    uint32_t frames, uint32_t tokens_per_frame, uint32_t block_size, int kind,
+                                    int sink, uint32_t temporal_window, uint32_t spatial_window,
+                                    const int* devices, int num_devices) {
+    if (!devices || num_devices < 1) return fail(RADIAL_ERR_INVALID, "attn_fwd_host_multi: no devices");
+    int rc = check_attn(q, k, v, o, heads, n, head_dim);
+    if (rc) return rc;
+    if ((rc = check_shape(frames, tokens_per_frame, block_size))) return rc;
+    if (static_cast<uint64_t>(frames) * tokens_per_frame != n)
+        return fail(RADIAL_ERR_INVALID, "masked_attention: layout shape mismatch");
+    // one host thread per device, heads split evenly (the split of heads.head_slice); each
+    // thread builds the (shared, static) mask on its device and runs the host-buffer pipeline
+    // on its slice of the host tensors -- the head-parallel path without torch / torchrun
+    const uint32_t ndev = static_cast<uint32_t>(num_devices);
+    std::vector<int> rcs(ndev, RADIAL_OK);
+    std::vector<std::string> msgs(ndev);
+    auto work = [&](uint32_t r) {
+        const uint32_t base = heads / ndev, rem = heads % ndev;
+        const uint32_t h0 = r * base + std::min(r, rem), hn = base + (r < rem ? 1u : 0u);
+        if (hn == 0) return;
+        int e = RADIAL_OK;
+        radial_layout* L = nullptr;
+        if (cudaSetDevice(devices[r]) != cudaSuccess) {
+            rcs[r] = fail(RADIAL_ERR_CUDA, "attn_fwd_host_multi: cudaSetDevice failed");
+        } else if ((e = radial_cuda_mask_build(frames, tokens_per_frame, block_size, kind, sink, temporal_window,
+                                               spatial_window, nullptr, &L)) != RADIAL_OK) {
+            rcs[r] = e;
+        } else {
+            const size_t hb = static_cast<size_t>(n) * head_dim * 2 * h0;
+            e = radial_cuda_attn_fwd_host(static_cast<const uint8_t*>(q) + hb, static_cast<const uint8_t*>(k) + hb,
+                                          static_cast<const uint8_t*>(v) + hb, static_cast<uint8_t*>(o) + hb,
+                                          lse ? lse + static_cast<size_t>(n) * h0 : nullptr, hn, n, head_dim, scale, L,
+                                          nullptr);
+            rcs[r] = e;
+            radial_cuda_layout_free(L);
+        }
+        if (rcs[r] != RADIAL_OK) msgs[r] = g_last_error;
+    };
+    int cur = 0;
+    cudaGetDevice(&cur);
+    std::vector<std::thread> th;
+    for (uint32_t r = 1; r < ndev; ++r) th.emplace_back(work, r);
+    work(0);
+    for (auto& t : th) t.join();
+    cudaSetDevice(cur);
+    for (uint32_t r = 0; r < ndev; ++r)
+        if (rcs[r] != RADIAL_OK) return fail(rcs[r], msgs[r]);
+    return RADIAL_OK;
 }
 
 int radial_cuda_attn_fwd_token_host(const void* q, const void* k, const void* v, void* o, float* lse,

@@ -231,6 +231,30 @@ def test_scatter_epilogue_writes_every_destination(P):
     assert torch.equal(lse, lse_ref)
 
 
+def test_host_multi_device_entry_matches_single_call(P):
+    """radial_cuda_attn_fwd_host_multi (one host thread per listed device, heads split
+    evenly, mask built per device) equals the single-device forward; device 0 listed twice
+    stands in for two GPUs (two threads, two pipelines, one device)."""
+    import ctypes
+    import torch
+    f, s, B, d, H = 6, 500, 128, 128, 5
+    n = f * s
+    g = torch.Generator(device="cuda").manual_seed(8)
+    q, k, v = (torch.randn(H, n, d, device="cuda", generator=g).to(torch.bfloat16) for _ in range(3))
+    lay = P.device_layout(P.GridShape(f, s), P.PatternSpec.radial(), B)
+    o_ref, lse_ref = P.masked_attention(q, k, v, lay, return_lse=True)
+    hq, hk, hv = (x.cpu().pin_memory() for x in (q, k, v))
+    for devs in ([0], [0, 0]):
+        ho = torch.empty_like(hq).pin_memory()
+        hl = torch.empty(H, n, dtype=torch.float32).pin_memory()
+        arr = (ctypes.c_int * len(devs))(*devs)
+        rc = P._lib.radial_cuda_attn_fwd_host_multi(hq.data_ptr(), hk.data_ptr(), hv.data_ptr(), ho.data_ptr(),
+                                                   hl.data_ptr(), H, n, d, 0.0, f, s, B, 0, 1, 0, 0, arr, len(devs))
+        assert rc == 0, P._lib.radial_cuda_last_error()
+        assert torch.equal(ho, o_ref.cpu()), devs
+        assert torch.equal(hl, lse_ref.cpu()), devs
+
+
 def test_fused_reassembly_through_symmetric_memory():
     """The multi-rank plumbing of the fused reassembly (torch symmetric memory rendezvous,
     peer pointers, barrier) under torchrun with the ranks this box has (1 here): every
