@@ -579,3 +579,41 @@ def masked_attention_backward(q, k, v, o, lse, dout, layout, scale: Optional[flo
                                      dv.data_ptr(), H, n, d, float(scale or 0.0), L.handle,
                                      ws.data_ptr(), _stream_ptr(stream)))
     return dq, dk, dv
+
+
+def _radial_attention_function():
+    """torch.autograd.Function over K2 (forward) and K3 (backward), built lazily so that
+    importing the package does not require torch."""
+    global _RadialAttnFn
+    if _RadialAttnFn is not None:
+        return _RadialAttnFn
+    import torch
+
+    class RadialAttentionFn(torch.autograd.Function):
+        @staticmethod
+        def forward(ctx, q, k, v, layout, scale):
+            q, k, v = (x.contiguous() for x in (q, k, v))
+            o, lse = masked_attention(q, k, v, layout, scale, return_lse=True)
+            ctx.save_for_backward(q, k, v, o, lse)
+            ctx.layout, ctx.scale = layout, scale
+            return o
+
+        @staticmethod
+        def backward(ctx, do):
+            q, k, v, o, lse = ctx.saved_tensors
+            dq, dk, dv = masked_attention_backward(q, k, v, o, lse, do.contiguous(), ctx.layout, ctx.scale)
+            return dq, dk, dv, None, None
+
+    _RadialAttnFn = RadialAttentionFn
+    return _RadialAttnFn
+
+
+_RadialAttnFn = None
+
+
+def radial_attention(q, k, v, layout, scale: Optional[float] = None):
+    """Differentiable radial attention for training (the paper's LoRA length-extension
+    tuning): O = masked_attention(q, k, v, layout) with autograd through the
+    K3 backward.  q, k, v bf16 CUDA [heads, n, head_dim] (head_dim 64 / 128, block 128 for
+    the backward); gradients come back bf16 in the same layout."""
+    return _radial_attention_function().apply(q, k, v, layout, scale)

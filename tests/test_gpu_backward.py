@@ -178,3 +178,34 @@ def test_backward_random_shape_fuzz(P):
         _check_blocks(dq[0].float().cpu().numpy(), wq, B, f"dQ {tag}")
         _check_blocks(dk[0].float().cpu().numpy(), wk, B, f"dK {tag}")
         _check_blocks(dv[0].float().cpu().numpy(), wv, B, f"dV {tag}")
+
+
+def test_autograd_function_trains_through_k3(P):
+    """radial_attention (torch.autograd.Function over K2 / K3): gradients of a scalar loss
+    through a small projection match the torch fp32 autograd of the dense masked softmax."""
+    import torch
+    f, s, d, H, B = 6, 256, 128, 2, 128
+    n = f * s
+    g = torch.Generator(device="cuda").manual_seed(9)
+    x = torch.randn(H, n, d, device="cuda", generator=g)
+    w = (torch.randn(d, d, device="cuda", generator=g) / d ** 0.5).requires_grad_(True)
+    lay = P.device_layout(P.GridShape(f, s), P.PatternSpec.radial(), B)
+
+    def proj(t):
+        return (t @ w).to(torch.bfloat16)
+    q, k, v = proj(x), proj(x.flip(1)), proj(x * 0.5)
+    loss = P.radial_attention(q, k, v, lay).float().pow(2).mean()
+    loss.backward()
+    gw = w.grad.clone()
+    w.grad = None
+    host = lay.host()
+    mask = torch.zeros(n, n, dtype=torch.bool, device="cuda")
+    for I in range(host.grid_rows):
+        for J in host.col_idx[host.row_ptr[I]:host.row_ptr[I + 1]]:
+            mask[I * B:(I + 1) * B, int(J) * B:(int(J) + 1) * B] = True
+    qf, kf, vf = proj(x).float(), proj(x.flip(1)).float(), proj(x * 0.5).float()
+    sc = ((qf @ kf.transpose(1, 2)) / d ** 0.5).masked_fill(~mask, float("-inf"))
+    ref = (torch.softmax(sc, -1) @ vf).pow(2).mean()
+    ref.backward()
+    rel = ((gw - w.grad).norm() / w.grad.norm()).item()
+    assert rel < 2e-2, rel
