@@ -429,3 +429,44 @@ extern "C" int radial_cuda_debug_exp_phase(int np, int iters, int warps, unsigne
         default: return RADIAL_ERR_INVALID;
     }
 }
+
+// ---------------------------------------------------------------------------
+// fp32 reduction-to-L2 throughput (diagnostic hook): every CTA adds a 128 x 128 fp32 tile
+// (one warp instruction = 32 consecutive floats of one row, red.global.add.f32) into a
+// [rows x 128] buffer at a pseudo-random 128-row block, `tiles` times; reports SM clocks.
+// mode 0: scalar red.add.f32; mode 1: red.global.add.v4.f32 (4 consecutive floats per lane).
+// ---------------------------------------------------------------------------
+namespace {
+template <int MODE>
+__global__ void red_rate_kernel(float* buf, uint32_t blocks, int tiles, unsigned long long* out) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const unsigned long long t0 = clock64();
+    uint32_t x = blockIdx.x * 2654435761u + 12345u;
+    for (int t = 0; t < tiles; ++t) {
+        x = x * 1664525u + 1013904223u;
+        float* tile = buf + static_cast<size_t>(x % blocks) * 128 * 128;
+        // 8 warps x 16 rows each
+        for (int r = warp * 16; r < warp * 16 + 16; ++r) {
+            if constexpr (MODE == 0) {
+#pragma unroll
+                for (int c = 0; c < 128; c += 32) atomicAdd(tile + r * 128 + c + lane, 1.0f);
+            } else {
+                float* a = tile + r * 128 + lane * 4;
+                asm volatile("red.global.add.v4.f32 [%0], {%1, %1, %1, %1};" ::"l"(a), "f"(1.0f) : "memory");
+            }
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) out[blockIdx.x] = clock64() - t0;
+}
+}  // namespace
+
+extern "C" int radial_cuda_debug_red_rate(int mode, float* buf, uint32_t blocks, int tiles, unsigned long long* out) {
+    if (mode == 0)
+        red_rate_kernel<0><<<148, 256>>>(buf, blocks, tiles, out);
+    else
+        red_rate_kernel<1><<<148, 256>>>(buf, blocks, tiles, out);
+    RADIAL_CUDA_TRY(cudaGetLastError());
+    RADIAL_CUDA_TRY(cudaDeviceSynchronize());
+    return RADIAL_OK;
+}
