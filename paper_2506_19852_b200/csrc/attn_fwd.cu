@@ -78,7 +78,10 @@ constexpr int kBQ = 128;        // query rows per tile
 // (K_j) or 2j + 1 (V_j) lives in slot t % kSlots.  The MMA issue order frees them in the
 // same order (K_j after S_B(j), V_j after PV_B(j)), so one ring suffices and every tile
 // is prefetched kSlots / 2 steps ahead (the L2 -> SM latency under load is ~1 step).
-constexpr int kSlots = 5;  // the MMA loop is unrolled by kSlots steps (constant slot indices)
+#ifndef RADIAL_FWD_SLOTS
+#define RADIAL_FWD_SLOTS 5
+#endif
+constexpr int kSlots = RADIAL_FWD_SLOTS;  // the MMA loop is unrolled by kSlots steps (constant slot indices)
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
 #ifndef RADIAL_P_PARTS
 #define RADIAL_P_PARTS 2
@@ -358,11 +361,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (j < L) FWD_COMMIT(&bar_empty[KSL]);
             };
             for (uint32_t j = 0; j <= L; j += kSlots) {
-                step(j, std::integral_constant<int, 0>{});
-                if (j + 1 <= L) step(j + 1, std::integral_constant<int, 1>{});
-                if (j + 2 <= L) step(j + 2, std::integral_constant<int, 2>{});
-                if (j + 3 <= L) step(j + 3, std::integral_constant<int, 3>{});
-                if (j + 4 <= L) step(j + 4, std::integral_constant<int, 4>{});
+                static_for<kSlots>([&](auto PC) {
+                    if (j + decltype(PC)::value <= L) step(j + decltype(PC)::value, PC);
+                });
             }
             FWD_COMMIT(&bar_ofull[0]);
             FWD_COMMIT(&bar_ofull[1]);
@@ -644,7 +645,10 @@ int make_tmap_bf16_3d(CUtensorMap* m, const void* base, uint64_t n, uint32_t D, 
     cuuint32_t estr[3] = {1, 1, 1};
     CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides,
                     box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+#ifndef RADIAL_TMA_L2_PROMO
+#define RADIAL_TMA_L2_PROMO CU_TENSOR_MAP_L2_PROMOTION_L2_256B
+#endif
+                    RADIAL_TMA_L2_PROMO, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return fail(RADIAL_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(r));
     return RADIAL_OK;
 }
