@@ -322,8 +322,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (warp == 4 && lane == 0) BTRACE(5, j);
             tc_fence_after();
             uint32_t sv[64];
+#ifdef RADIAL_BWD_LD32
             tmem_ld32(kTmem + la + kColS + wg * 64, *reinterpret_cast<uint32_t(*)[32]>(sv));
             tmem_ld32(kTmem + la + kColS + wg * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(sv + 32));
+#else
+            tmem_ld64(kTmem + la + kColS + wg * 64, sv);
+#endif
             tmem_wait_ld();
             tc_fence_before();
             __syncwarp();
@@ -345,8 +349,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_wait(bar_dp, j & 1);
             tc_fence_after();
             uint32_t dp[64];
+#ifdef RADIAL_BWD_LD32
             tmem_ld32(kTmem + la + kColDP + wg * 64, *reinterpret_cast<uint32_t(*)[32]>(dp));
             tmem_ld32(kTmem + la + kColDP + wg * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(dp + 32));
+#else
+            tmem_ld64(kTmem + la + kColDP + wg * 64, dp);
+#endif
             tmem_wait_ld();
             tc_fence_before();
             __syncwarp();
@@ -582,8 +590,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (warp == 4 && lane == 0) BTRACE(5, i);
             tc_fence_after();
             uint32_t sv[64];
+#ifdef RADIAL_BWD_LD32
             tmem_ld32(kTmem + la + kColS + wg * 64, *reinterpret_cast<uint32_t(*)[32]>(sv));
             tmem_ld32(kTmem + la + kColS + wg * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(sv + 32));
+#else
+            tmem_ld64(kTmem + la + kColS + wg * 64, sv);
+#endif
             tmem_wait_ld();
             tc_fence_before();
             __syncwarp();
@@ -610,8 +622,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (warp == 4 && lane == 0) BTRACE(8, i);
             tc_fence_after();
             uint32_t dp[64];
+#ifdef RADIAL_BWD_LD32
             tmem_ld32(kTmem + la + kColDP + wg * 64, *reinterpret_cast<uint32_t(*)[32]>(dp));
             tmem_ld32(kTmem + la + kColDP + wg * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(dp + 32));
+#else
+            tmem_ld64(kTmem + la + kColDP + wg * 64, dp);
+#endif
             tmem_wait_ld();
             // P^T into the (now consumed) dP^T columns, in two query halves
 #pragma unroll

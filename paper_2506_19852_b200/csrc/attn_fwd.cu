@@ -399,7 +399,16 @@ __global__ void __launch_bounds__(kThreads, 1)
             sphase ^= 1;
             tc_fence_after();
             float s[BK];
-            // first half, wait, then the second half's load overlaps the first half's max
+            // first half, wait, then the second half's load overlaps the first half's max; one
+            // 64-column tcgen05.ld per half (+1.5% over two 32-column loads)
+#if !defined(RADIAL_FWD_LD32)
+            if constexpr (BK == 128) {
+                uint32_t u[64];
+                tmem_ld64(s_addr, u);
+#pragma unroll
+                for (int x = 0; x < 64; ++x) s[x] = __uint_as_float(u[x]);
+            } else
+#endif
 #pragma unroll
             for (int c = 0; c < BK / 2; c += 32) {
                 uint32_t u[32];
@@ -411,6 +420,14 @@ __global__ void __launch_bounds__(kThreads, 1)
             float mh[8];
 #pragma unroll
             for (int x = 0; x < 8; ++x) mh[x] = s[x];
+#if !defined(RADIAL_FWD_LD32)
+            if constexpr (BK == 128) {
+                uint32_t u[64];
+                tmem_ld64(s_addr + 64, u);
+#pragma unroll
+                for (int x = 0; x < 64; ++x) s[64 + x] = __uint_as_float(u[x]);
+            } else
+#endif
 #pragma unroll
             for (int c = BK / 2; c < BK; c += 32) {
                 uint32_t u[32];
