@@ -12,15 +12,18 @@
 //
 // Warp roles (384 threads, one CTA per SM):
 //   warp 0      TMA producer: Q tiles once, then K_j, V_j into one 5-slot ring
-//   warp 1      MMA issuer (one thread): S_t = Q_t K_j^T (SS, both operands
-//               K-major in smem) and O_t += P_t V_j (TS: P from TMEM, V
-//               MN-major in smem), tcgen05.commit -> mbarriers
+//   warp 1      MMA issuer (converged warp, elected lane, four K-steps per asm
+//               block): S_t = Q_t K_j^T (SS, both operands K-major in smem) and
+//               O_t += P_t V_j (TS: P from TMEM, V MN-major in smem),
+//               tcgen05.commit -> mbarriers
 //   warp 2      TMEM allocator (512 columns: S0 | S1 | O0 | O1)
 //   warps 4-7   softmax + epilogue for Q tile 0 (one thread per row = TMEM lane)
 //   warps 8-11  softmax + epilogue for Q tile 1
 // P (bf16) is written over its own S columns with tcgen05.st; the MMA issue
 // order (PV_t(j-1) before S_t(j)) makes that alias safe.  Online softmax in
-// the exp2 domain with lazy (threshold 8) rescaling of O in TMEM.
+// the exp2 domain with lazy (threshold 8) rescaling of O in TMEM.  Optionally the
+// epilogue stores O rows straight into several ranks' full-O buffers (fused
+// head-parallel reassembly, radial_cuda_attn_fwd_scatter).
 #include <cmath>
 #include <type_traits>
 
