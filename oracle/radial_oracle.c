@@ -11,6 +11,11 @@
  * pinned against the reference itself (oracle/_ref, built from the
  * reference headers by oracle/Makefile) and against the golden sha256
  * vectors of SURVEY.md section 8c (tests/golden/layouts.json).
+ *
+ * The backward restatement (ro_attention_bwd) has no reference counterpart (the
+ * reference has no gradient code): its parity is unpinned by the
+ * reference and is cross-checked only against torch float64 autograd and
+ * finite differences (tests/test_oracle.py).
  */
 #include <math.h>
 #include <pthread.h>
