@@ -209,3 +209,17 @@ def test_autograd_function_trains_through_k3(P):
     ref.backward()
     rel = ((gw - w.grad).norm() / w.grad.norm()).item()
     assert rel < 2e-2, rel
+
+
+def test_kernels_are_deterministic_run_to_run():
+    """No atomics, fixed reduction order: repeated forward / token-exact forward / backward
+    calls must be bit-identical (a race in the barrier protocol would show up here)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    for cfg, iters in (("mochi28", 6), ("tiny", 40)):
+        r = subprocess.run([sys.executable, os.path.join(root, "scripts", "stress_determinism.py"),
+                            "--config", cfg, "--iters", str(iters)], capture_output=True, text=True, timeout=300)
+        assert r.returncode == 0, r.stdout + r.stderr[-3000:]
+        assert '"mismatches": {}' in r.stdout
