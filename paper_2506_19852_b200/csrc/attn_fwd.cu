@@ -47,8 +47,7 @@ __device__ unsigned long long* g_trace = nullptr;
 constexpr int kTraceCtas = 4, kTraceSteps = 64, kTraceEv = 24;
 #define TRACE(ev, j)                                                                         \
     do {                                                                                     \
-        if (g_trace && blockIdx.x < kTraceCtas && (j) < kTraceSteps)                          \
-            g_trace[(blockIdx.x * kTraceSteps + (j)) * kTraceEv + (ev)] = clock64();         \
+        if (trace_base && (j) < kTraceSteps) trace_base[(j) * kTraceEv + (ev)] = clock64();   \
     } while (0)
 #else
 #define TRACE(ev, j) \
@@ -160,6 +159,11 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
+#ifdef RADIAL_TRACE
+    // loaded once: a global load per event would perturb the timeline it measures
+    unsigned long long* const trace_base =
+        (g_trace && blockIdx.x < kTraceCtas) ? g_trace + blockIdx.x * kTraceSteps * kTraceEv : nullptr;
+#endif
 
     // work item: head-major so the CTAs resident at any time share one head's K/V in L2
     // (K+V of a head = 2 n d bytes = 61 MB at n = 118,800); longest chunks first within a
@@ -225,6 +229,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const uint32_t slot = t % kSlots;
                 mbar_wait(&bar_empty[slot], ((t / kSlots) & 1) ^ 1);
                 TRACE(18 + (t & 1), t >> 1);
+#ifdef RADIAL_FWD_NO_LOADS
+                mbar_arrive(&bar_full[slot]);  // timing experiment: stale K/V tiles
+                continue;
+#endif
                 mbar_arrive_expect_tx(&bar_full[slot], Cfg::kKVBytes);
                 uint8_t* dst = smem + Cfg::kSmemKV + slot * Cfg::kKVBytes;
                 const CUtensorMap* tm = (t & 1) ? &tm_v : &tm_k;
@@ -280,6 +288,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 // every union entry keeps a block of at least one tile, so V_{j-1} is always
                 // consumed; it is waited for and released unconditionally (no TMA in flight
                 // into a released slot)
+                TRACE(20, j);
                 if (j > 0) mbar_wait(&bar_full[VSL], ((2 * j - 1) / kSlots) & 1);
                 TRACE(17, j);
                 tc_fence_after();
@@ -344,6 +353,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     pend0 = false;
                 }
                 if (j < L) {
+                    TRACE(21, j);
                     mbar_wait(&bar_full[KSL], ((2 * j) / kSlots) & 1);
                     TRACE(16, j);
                     tc_fence_after();
@@ -401,6 +411,15 @@ __global__ void __launch_bounds__(kThreads, 1)
             if ((warp & 3) == 0 && lane == 0) TRACE(4 * t + 1, j);
             sphase ^= 1;
             tc_fence_after();
+#ifdef RADIAL_FWD_MMA_ONLY
+            // timing experiment: no softmax at all (P = stale TMEM contents); measures the
+            // MMA + TMA pipeline alone
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0)
+                for (int h = 0; h < kPParts; ++h) mbar_arrive(&bar_pready[kPParts * t + h]);
+            continue;
+#endif
             float s[BK];
             // first half, wait, then the second half's load overlaps the first half's max; one
             // 64-column tcgen05.ld per half (+1.5% over two 32-column loads)

@@ -202,6 +202,100 @@ extern "C" int radial_cuda_debug_mma_rate(int mode, int iters, int ctas, unsigne
 }
 
 // ---------------------------------------------------------------------------
+// Forward MMA-issue pattern microbenchmark (diagnostic hook): one thread issues, per
+// step, the forward kernel's MMA sequence without waiting for anything:
+//   MIX 0: 16 SS 128x128x16 MMAs (S only)
+//   MIX 1: PV_A (8 TS into O_A, A = P_A from TMEM), S_A (8 SS into S_A), PV_B, S_B
+// plus COMMITS tcgen05.commit per step (to barriers nobody waits on) spread over the step.
+// Reports SM clocks for `iters` steps.
+// ---------------------------------------------------------------------------
+namespace {
+template <int MIX, int COMMITS>
+__global__ void __launch_bounds__(128, 1) mma_mix_kernel(int iters, unsigned long long* out) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                               ~static_cast<uintptr_t>(1023));
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + 96 * 1024);
+    uint32_t* slot = reinterpret_cast<uint32_t*>(bar + 9);
+    const int warp = threadIdx.x >> 5;
+    for (int i = threadIdx.x; i < 96 * 1024 / 16; i += blockDim.x)
+        reinterpret_cast<uint4*>(smem)[i] = make_uint4(0x3c003c00u, 0, 0x3c003c00u, 0);
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < 9; ++i) mbar_init(&bar[i], 1);
+        fence_barrier_init();
+    }
+    if (warp == 1) tmem_alloc(slot, 512);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    if (*slot != 0) __trap();
+    constexpr uint32_t tmem = 0;
+    if (threadIdx.x == 0) {
+        const uint32_t q = smem_u32(smem), kv = smem_u32(smem + 64 * 1024);
+        constexpr uint32_t idS = idesc_bf16(128, 128, 0, 0), idO = idesc_bf16(128, 128, 0, 1);
+        int c = 0;
+        auto commit = [&](int part) {
+            // COMMITS commits per step, issued after parts 0..3 as evenly as possible
+            constexpr int per = COMMITS;
+            for (int x = 0; x < per; ++x)
+                if ((x * 4) / (per ? per : 1) == part) mma_commit(&bar[(c++) & 7]);
+        };
+        const unsigned long long t0 = clock64();
+        for (int it = 0; it < iters; ++it) {
+#pragma unroll
+            for (int part = 0; part < 4; ++part) {
+                const int T = part >> 1;
+                if (MIX == 0 || (part & 1)) {
+#pragma unroll
+                    for (int kk = 0; kk < 8; ++kk)
+                        mma_ss(tmem + T * 128, sdesc_sw128(q + T * 32768 + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024),
+                               sdesc_sw128(kv + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024), idS, kk ? 1u : 0u);
+                } else {
+#pragma unroll
+                    for (int kk = 0; kk < 8; ++kk)
+                        mma_ts(tmem + 256 + T * 128, tmem + T * 128 + kk * 8,
+                               sdesc_sw128(kv + kk * 2048, 128 * 128 / 2, 1024), idO, 1u);
+                }
+                commit(part);
+            }
+        }
+        mma_commit(&bar[8]);  // completes when every MMA above has finished
+        mbar_wait(&bar[8], 0);
+        const unsigned long long t1 = clock64();
+        out[blockIdx.x] = (t1 - t0);
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        tmem_dealloc(*slot, 512);
+    }
+}
+template <int MIX, int COMMITS>
+int run_mix(int iters, unsigned long long* out_dev) {
+    const int smem = 96 * 1024 + 128 + 1024;
+    auto k = mma_mix_kernel<MIX, COMMITS>;
+    RADIAL_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    k<<<148, 128, smem>>>(iters, out_dev);
+    RADIAL_CUDA_TRY(cudaGetLastError());
+    RADIAL_CUDA_TRY(cudaDeviceSynchronize());
+    return RADIAL_OK;
+}
+}  // namespace
+
+// mode: 0 S-only, 1 fwd mix; commits per step 0, 2, 4, 8
+extern "C" int radial_cuda_debug_mma_mix(int mode, int commits, int iters, unsigned long long* out_dev) {
+    if (mode == 0 && commits == 0) return run_mix<0, 0>(iters, out_dev);
+    if (mode == 0 && commits == 4) return run_mix<0, 4>(iters, out_dev);
+    if (mode == 1 && commits == 0) return run_mix<1, 0>(iters, out_dev);
+    if (mode == 1 && commits == 2) return run_mix<1, 2>(iters, out_dev);
+    if (mode == 1 && commits == 4) return run_mix<1, 4>(iters, out_dev);
+    if (mode == 1 && commits == 8) return run_mix<1, 8>(iters, out_dev);
+    return RADIAL_ERR_INVALID;
+}
+
+// ---------------------------------------------------------------------------
 // Elementwise pipe-rate microbenchmark (diagnostic hook): 148 CTAs x `warps`
 // warps, each thread runs 8 independent chains of one instruction kind and
 // reports SM clocks for `iters` x 8 instructions per thread.

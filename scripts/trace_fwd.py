@@ -28,7 +28,7 @@ def main():
     torch.cuda.synchronize()
     t = buf.view(CT, ST, EV).cpu().numpy().astype(np.int64)
     names = ["A.wait", "A.S", "A.P0", "A.P1", "B.wait", "B.S", "B.P0", "B.P1",
-             "M.PA0", "M.PA1", "M.PB0", "M.PB1", "M.SA", "M.SB", "A.ld", "A.max", "M.kfull", "M.vfull", "L.K", "L.V"]
+             "M.PA0", "M.PA1", "M.PB0", "M.PB1", "M.SA", "M.SB", "A.ld", "A.max", "M.kfull", "M.vfull", "L.K", "L.V", "M.vw0", "M.kw0"]
     for c in range(CT):
         base = t[c, 1, 1]
         print(f"CTA {c}: times relative to step-1 A.S (clk)")
