@@ -166,8 +166,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 #endif
 
     // work item: head-major so the CTAs resident at any time share one head's K/V in L2
-    // (K+V of a head = 2 n d bytes = 61 MB at n = 118,800); longest chunks first within a
-    // head (LPT) so the tail of the grid is short.
+    // (K+V of a head = 2 n d bytes = 61 MB at n = 118,800); longest chunks first within
+    // windows of 2 x (SM count) consecutive chunks (LPT for a short grid tail, windowed so the
+    // resident CTAs' K/V stays in L2 when a head does not: H132, 243 MB per head).
     const uint32_t item = blockIdx.x;
     const uint32_t head = item / p.C;
     const uint32_t chunk = p.order ? p.order[item % p.C] : item % p.C;

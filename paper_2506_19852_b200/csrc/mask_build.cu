@@ -215,18 +215,24 @@ __global__ void __launch_bounds__(1024) scan_rows(const uint32_t* __restrict__ c
     }
 }
 
-// Stable argsort of rows by list length, longest first (LPT work order), one CTA.
-// keys = ptr[i+1] - ptr[i]; n <= kSortMax (bitonic sort in shared memory).
+// Stable argsort of lists by length, longest first (LPT work order) inside windows of
+// `window` consecutive lists, one CTA.  keys = ptr[i+1] - ptr[i]; n <= kSortMax (bitonic sort
+// in shared memory).  Windowing keeps the CTAs resident at any time on neighbouring query
+// blocks, whose K/V working set stays in L2: at H132 (243 MB of K+V per head) a global LPT
+// order streams the whole head from DRAM and the power-capped clock drops (measured: 591 ->
+// 547 ms forward, 1707 -> 1562 ms backward with windows of 2 x 148 lists; H33 unchanged).
 constexpr int kSortMax = 4096;  // 32 KB of static shared memory
 __global__ void __launch_bounds__(1024) lpt_sort_kernel(const uint64_t* __restrict__ ptr, uint32_t n,
-                                                        uint32_t* __restrict__ order) {
-    __shared__ unsigned long long key[kSortMax];  // (max_len - len) << 32 | index: ascending sort
+                                                        uint32_t window, uint32_t* __restrict__ order) {
+    __shared__ unsigned long long key[kSortMax];  // window << 52 | (max_len - len) << 32 | index
     uint32_t m = 1;
     while (m < n) m <<= 1;
     for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) {
         if (i < n) {
             const uint64_t len = ptr[i + 1] - ptr[i];
-            key[i] = (static_cast<unsigned long long>(0xffffffffu - static_cast<uint32_t>(len)) << 32) | i;
+            const uint32_t l20 = static_cast<uint32_t>(len < 0xfffffu ? len : 0xfffffu);
+            key[i] = (static_cast<unsigned long long>(i / window) << 52) |
+                     (static_cast<unsigned long long>(0xfffffu - l20) << 32) | i;
         } else {
             key[i] = ~0ull;
         }
@@ -269,12 +275,17 @@ int fill(F pred, uint32_t rows, uint32_t cols, const uint64_t* ptr, uint32_t* id
     return RADIAL_OK;
 }
 
-// Longest-processing-time-first order of `n` lists (device sort; host fallback when large).
+// Longest-processing-time-first order of `n` lists within windows of 2 x (SM count) lists
+// (device sort; host fallback when large).
 int lpt_order(const uint64_t* dptr, uint32_t n, cudaStream_t st, uint32_t** order_out) {
     RADIAL_CUDA_TRY(cudaMallocAsync(order_out, sizeof(uint32_t) * std::max<uint32_t>(n, 1), st));
     if (n == 0) return RADIAL_OK;
+    int dev = 0, sms = 148;
+    RADIAL_CUDA_TRY(cudaGetDevice(&dev));
+    RADIAL_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    const uint32_t window = 2u * static_cast<uint32_t>(std::max(sms, 1));
     if (n <= static_cast<uint32_t>(kSortMax)) {
-        lpt_sort_kernel<<<1, 1024, 0, st>>>(dptr, n, *order_out);
+        lpt_sort_kernel<<<1, 1024, 0, st>>>(dptr, n, window, *order_out);
         RADIAL_CUDA_TRY(cudaGetLastError());
         return RADIAL_OK;
     }
@@ -283,8 +294,10 @@ int lpt_order(const uint64_t* dptr, uint32_t n, cudaStream_t st, uint32_t** orde
     RADIAL_CUDA_TRY(cudaStreamSynchronize(st));
     std::vector<uint32_t> ord(n);
     std::iota(ord.begin(), ord.end(), 0u);
-    std::stable_sort(ord.begin(), ord.end(),
-                     [&](uint32_t a, uint32_t b) { return (h[a + 1] - h[a]) > (h[b + 1] - h[b]); });
+    std::stable_sort(ord.begin(), ord.end(), [&](uint32_t a, uint32_t b) {
+        if (a / window != b / window) return a < b;
+        return (h[a + 1] - h[a]) > (h[b + 1] - h[b]);
+    });
     RADIAL_CUDA_TRY(cudaMemcpyAsync(*order_out, ord.data(), sizeof(uint32_t) * n, cudaMemcpyHostToDevice, st));
     RADIAL_CUDA_TRY(cudaStreamSynchronize(st));
     return RADIAL_OK;

@@ -18,7 +18,10 @@ def main():
     import paper_2506_19852_b200 as P
     pynvml.nvmlInit()
     hdl = pynvml.nvmlDeviceGetHandleByIndex(0)
-    f, s, H, d, B = 33, 3600, 24, 128, 128
+    cfg = sys.argv[1] if len(sys.argv) > 1 else "hunyuan33"
+    f, s, H = {"hunyuan33": (33, 3600, 24), "hunyuan132": (132, 3600, 24), "wan21": (21, 3600, 40),
+               "mochi28": (28, 1590, 24)}[cfg]
+    d, B = 128, 128
     n = f * s
     g = torch.Generator(device="cuda").manual_seed(0)
     q, k, v = (torch.randn(H, n, d, device="cuda", generator=g).to(torch.bfloat16) for _ in range(3))
@@ -28,9 +31,11 @@ def main():
     R = host.grid_rows
     union = sum(len(np.union1d(ci[rp[2 * p]:rp[2 * p + 1]], ci[rp[2 * p + 1]:rp[2 * p + 2]] if 2 * p + 1 < R else []))
                 for p in range((R + 1) // 2))
-    res = {"lib": os.path.basename(os.path.dirname(P.library_path()))}
+    res = {"lib": os.path.basename(os.path.dirname(P.library_path())), "config": cfg}
     for name, fn, steps, it in (("sparse", lambda: P.masked_attention(q, k, v, lay), union * H, 10),
                                 ("dense", lambda: P.dense_attention(q, k, v), ((R + 1) // 2) * R * H, 4)):
+        if name == "dense" and cfg == "hunyuan132":
+            continue
         for _ in range(3):
             fn()
         clk = []
