@@ -204,6 +204,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         tma_prefetch_desc(&tm_k);
         tma_prefetch_desc(&tm_v);
     }
+    if (threadIdx.x == 0) TRACE(22, 0);  // CTA start
     if (warp == 2) tmem_alloc(tmem_slot, Cfg::kTmemCols);
     tc_fence_before();
     __syncthreads();
@@ -607,7 +608,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             l += (r2a.x + r2a.y) + (r2b.x + r2b.y);
         }
         // ------------------------------------------------------------ epilogue
+        if (warp == 4 && lane == 0) TRACE(22, 2);  // tile 0 softmax done
         mbar_wait(&bar_ofull[t], 0);
+        if (warp == 4 && lane == 0) TRACE(22, 3);  // O final
         tc_fence_after();
         const float inv = l > 0.f ? 1.f / l : 0.f;
         __nv_bfloat16* orow = p.o + (static_cast<uint64_t>(head) * p.n + grow) * D;
@@ -648,6 +651,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_after();
         tmem_dealloc(*tmem_slot, Cfg::kTmemCols);
     }
+    if (threadIdx.x == 0) TRACE(22, 1);  // CTA end
 }
 
 using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
