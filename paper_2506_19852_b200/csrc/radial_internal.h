@@ -32,7 +32,7 @@ struct radial_layout {
     uint32_t G = 0, C = 0;        // blocks per chunk, number of chunks
     uint64_t* uptr = nullptr;     // [C+1]
     uint32_t* uidx = nullptr;
-    uint32_t* uorder = nullptr;   // chunks by descending list length (LPT)
+    uint32_t* uorder = nullptr;   // chunks by descending list length within windows (LPT)
     // Backward dK/dV work list: same over KV chunks using the CSC.
     uint64_t* tptr = nullptr;
     uint32_t* tidx = nullptr;
