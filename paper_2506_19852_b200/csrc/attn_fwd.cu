@@ -274,6 +274,10 @@ __global__ void __launch_bounds__(kThreads, 1)
 #endif
             };
             uint32_t e_next = L > 0 ? uentry(0) : 0u;
+            // tile B's pending PV is issued at step pv1_step (normally the step after its S; two
+            // steps after when its S was issued one entry early)
+            uint32_t pv1_step = 0;
+            bool b_done = false;  // the current entry's S_B was issued early, in the previous step
             // step j: PV_A(j-1), S_A(j), PV_B(j-1), S_B(j); each operand is waited for just
             // before its first use and released right after its last use.
             auto step = [&](uint32_t j, auto PC) {
@@ -281,11 +285,21 @@ __global__ void __launch_bounds__(kThreads, 1)
                 constexpr int KSL = (2 * PH) % kSlots;          // slot of K_j
                 constexpr int VSL = (2 * PH + kSlots - 1) % kSlots;  // slot of V_{j-1}
                 uint32_t tf0 = 0, tf1 = 0;
+                bool early = false;
                 if (j < L) {
                     const uint32_t m = e_next >> 28;  // entry(j), loaded one step ahead
                     if (j + 1 < L) e_next = uentry(j + 1);
                     tf0 = m & ((1u << Cfg::GT) - 1);
                     tf1 = (m >> Cfg::GT) & ((1u << Cfg::GT) - 1);
+#ifndef RADIAL_FWD_NO_EARLY_S
+                    // a tile-A-only entry followed by a tile-B-only one (the worklist pairs solo
+                    // entries up this way): issue the next entry's S_B now, so the two tiles'
+                    // softmaxes overlap as in a shared step
+                    if (tf0 && !tf1 && j + 1 < L) {
+                        const uint32_t mn = e_next >> 28;
+                        early = !(mn & ((1u << Cfg::GT) - 1)) && ((mn >> Cfg::GT) & ((1u << Cfg::GT) - 1));
+                    }
+#endif
                 }
                 // every union entry keeps a block of at least one tile, so V_{j-1} is always
                 // consumed; it is waited for and released unconditionally (no TMA in flight
@@ -326,8 +340,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                     pphase ^= 1;
                     acc = 1;
                 };
-                auto qk = [&](auto TC) {
+                auto qk = [&](auto TC, auto KC_) {
                     constexpr int T = decltype(TC)::value;
+                    constexpr int KSL = decltype(KC_)::value;  // slot of the K tile
                     constexpr uint32_t s_col = T ? Cfg::kColS1 : Cfg::kColS0;
 
 #if defined(RADIAL_FWD_WARP_MMA) && !defined(RADIAL_FWD_NO_GROUP)
@@ -361,17 +376,28 @@ __global__ void __launch_bounds__(kThreads, 1)
                     tc_fence_after();
                 }
                 if (tf0) {
-                    qk(std::integral_constant<int, 0>{});
+                    qk(std::integral_constant<int, 0>{}, std::integral_constant<int, KSL>{});
                     pend0 = true;
                 }
-                if (pend1) {
+                if (pend1 && pv1_step == j) {
                     pv(std::integral_constant<int, 1>{}, acc1, pphase1);
                     pend1 = false;
                 }
                 if (j > 0) FWD_COMMIT(&bar_empty[VSL]);  // V_{j-1} free once its PVs finish
-                if (tf1) {
-                    qk(std::integral_constant<int, 1>{});
+                if (tf1 && !b_done) {
+                    qk(std::integral_constant<int, 1>{}, std::integral_constant<int, KSL>{});
                     pend1 = true;
+                    pv1_step = j + 1;
+                }
+                b_done = false;
+                if (early) {
+                    constexpr int KSL1 = (2 * PH + 2) % kSlots;  // slot of K_{j+1}
+                    mbar_wait(&bar_full[KSL1], ((2 * j + 2) / kSlots) & 1);
+                    tc_fence_after();
+                    qk(std::integral_constant<int, 1>{}, std::integral_constant<int, KSL1>{});
+                    pend1 = true;
+                    pv1_step = j + 2;  // V_{j+1} is read at step j + 2
+                    b_done = true;
                 }
                 if (j < L) FWD_COMMIT(&bar_empty[KSL]);
             };

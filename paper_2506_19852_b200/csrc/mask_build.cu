@@ -257,6 +257,39 @@ __global__ void __launch_bounds__(1024) lpt_sort_kernel(const uint64_t* __restri
     for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) order[i] = static_cast<uint32_t>(key[i] & 0xffffffffu);
 }
 
+// Forward chunk lists: each entry kept by tile 0 only is followed by the next entry kept by
+// tile 1 only (pulled forward from later in the list), so the forward's MMA warp can issue
+// that entry's S together with the first and the two solo steps overlap like one shared
+// step.  Everything else stays in ascending J order (K/V locality in L2).  One thread per
+// chunk; `in` is a copy of the fill order.
+__global__ void __launch_bounds__(256) pair_solo_entries(const uint64_t* __restrict__ ptr, uint32_t C, uint32_t GT,
+                                                         const uint32_t* __restrict__ in, uint32_t* __restrict__ out) {
+    const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= C) return;
+    const uint64_t b = ptr[c], e = ptr[c + 1];
+    const uint32_t m0 = (1u << GT) - 1u;
+    auto kind = [&](uint32_t x) {  // 0 shared, 1 tile-0 only, 2 tile-1 only
+        const uint32_t m = x >> 28;
+        const bool a = m & m0, bb = (m >> GT) & m0;
+        return (a && bb) ? 0 : (a ? 1 : 2);
+    };
+    uint64_t o = b, nb = b;  // nb: one past the last tile-1-only entry pulled forward
+    for (uint64_t i = b; i < e; ++i) {
+        const uint32_t x = in[i];
+        const int k = kind(x);
+        if (k == 2 && i < nb) continue;  // already emitted behind a tile-0-only entry
+        out[o++] = x;
+        if (k == 1) {
+            uint64_t q = nb > i + 1 ? nb : i + 1;
+            while (q < e && kind(in[q]) != 2) ++q;
+            if (q < e) {
+                out[o++] = in[q];
+                nb = q + 1;
+            }
+        }
+    }
+}
+
 // One list family (rows x cols under predicate F): counts -> exclusive scan into ptr.
 template <class F>
 int count_and_scan(F pred, uint32_t rows, uint32_t cols, uint32_t* counts, uint64_t* ptr, ScanStats* dstats,
@@ -377,6 +410,14 @@ int build_worklists(radial_layout* L, cudaStream_t st) {
     RADIAL_CUDA_TRY(cudaMallocAsync(&L->uidx, sizeof(uint32_t) * std::max<uint64_t>(sc.host[2].nnz, 1), st));
     RADIAL_CUDA_TRY(cudaMallocAsync(&L->tidx, sizeof(uint32_t) * std::max<uint64_t>(sc.host[3].nnz, 1), st));
     if ((rc = fill(uq, C, R, L->uptr, L->uidx, 1, st))) return rc;
+    if (C && sc.host[2].nnz) {
+        uint32_t* tmp = nullptr;
+        RADIAL_CUDA_TRY(cudaMallocAsync(&tmp, sizeof(uint32_t) * sc.host[2].nnz, st));
+        RADIAL_CUDA_TRY(cudaMemcpyAsync(tmp, L->uidx, sizeof(uint32_t) * sc.host[2].nnz, cudaMemcpyDeviceToDevice, st));
+        pair_solo_entries<<<(C + 255) / 256, 256, 0, st>>>(L->uptr, C, L->G / 2, tmp, L->uidx);
+        RADIAL_CUDA_TRY(cudaGetLastError());
+        RADIAL_CUDA_TRY(cudaFreeAsync(tmp, st));
+    }
     if ((rc = fill(ukv, C, R, L->tptr, L->tidx, 1, st))) return rc;
     RADIAL_CUDA_TRY(cudaStreamSynchronize(st));
     return RADIAL_OK;
