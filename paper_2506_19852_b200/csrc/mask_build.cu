@@ -416,7 +416,7 @@ int build_worklists(radial_layout* L, cudaStream_t st) {
         RADIAL_CUDA_TRY(cudaMemcpyAsync(tmp, L->uidx, sizeof(uint32_t) * sc.host[2].nnz, cudaMemcpyDeviceToDevice, st));
         pair_solo_entries<<<(C + 255) / 256, 256, 0, st>>>(L->uptr, C, L->G / 2, tmp, L->uidx);
         RADIAL_CUDA_TRY(cudaGetLastError());
-        RADIAL_CUDA_TRY(cudaFreeAsync(tmp, st));
+        L->uidx_asc = tmp;  // kept for the token-exact forward (incremental key-frame tracking)
     }
     if ((rc = fill(ukv, C, R, L->tptr, L->tidx, 1, st))) return rc;
     RADIAL_CUDA_TRY(cudaStreamSynchronize(st));

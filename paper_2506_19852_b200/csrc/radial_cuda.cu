@@ -45,7 +45,8 @@ void free_layout(radial_layout* L) {
     // drain any in-flight kernel that may still read the layout
     cudaDeviceSynchronize();
     void* ptrs[] = {L->row_ptr, L->col_idx, L->col_ptr, L->row_idx, L->uptr,   L->uidx,
-                    L->uorder,  L->tptr,    L->tidx,    L->torder,  L->rorder, L->corder};
+                    L->uorder,  L->tptr,    L->tidx,    L->torder,  L->rorder, L->corder,
+                    L->uidx_asc};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     delete L;

@@ -33,6 +33,7 @@ struct radial_layout {
     uint64_t* uptr = nullptr;     // [C+1]
     uint32_t* uidx = nullptr;
     uint32_t* uorder = nullptr;   // chunks by descending list length within windows (LPT)
+    uint32_t* uidx_asc = nullptr; // the same entries in ascending J (token-exact mode); uidx pairs solo entries
     // Backward dK/dV work list: same over KV chunks using the CSC.
     uint64_t* tptr = nullptr;
     uint32_t* tidx = nullptr;
