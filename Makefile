@@ -1,19 +1,23 @@
 # Builds the product library (sm_100a) and the parity checker.
 #   make            -> paper_2506_19852_b200/lib/libradial_cuda.so + oracle
 #   make lib        -> CUDA library only
+#   make debug      -> diagnostics library (tcgen05 / pipe microbenchmarks, scripts/ only)
 NVCC ?= nvcc
 ARCH := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS := -O3 -std=c++17 $(ARCH) -lineinfo -Xcompiler -fPIC -Xptxas -v --expt-relaxed-constexpr
 CSRC := paper_2506_19852_b200/csrc
-SRCS := $(CSRC)/radial_cuda.cu $(CSRC)/mask_build.cu $(CSRC)/attn_fwd.cu $(CSRC)/attn_bwd.cu $(CSRC)/debug_mma.cu
+SRCS := $(CSRC)/radial_cuda.cu $(CSRC)/mask_build.cu $(CSRC)/attn_fwd.cu $(CSRC)/attn_bwd.cu
 HDRS := $(CSRC)/mask_rule.cuh $(CSRC)/sm100.cuh $(CSRC)/radial_internal.h include/radial_cuda.h
 LIB := paper_2506_19852_b200/lib/libradial_cuda.so
+DEBUG_LIB := paper_2506_19852_b200/lib/libradial_debug.so
 OBJDIR := build/obj
 OBJS := $(patsubst $(CSRC)/%.cu,$(OBJDIR)/%.o,$(SRCS))
 
-all: lib oracle
+all: lib debug oracle
 
 lib: $(LIB)
+
+debug: $(DEBUG_LIB)
 
 $(OBJDIR)/%.o: $(CSRC)/%.cu $(HDRS)
 	@mkdir -p $(OBJDIR)
@@ -23,14 +27,19 @@ $(LIB): $(OBJS)
 	@mkdir -p $(dir $@)
 	$(NVCC) $(ARCH) -shared -o $@ $(OBJS)
 
+# diagnostics only (never loaded by the product path); links the product library for the
+# shared tensor-map helper
+$(DEBUG_LIB): $(OBJDIR)/debug_mma.o $(LIB)
+	$(NVCC) $(ARCH) -shared -o $@ $(OBJDIR)/debug_mma.o -L$(dir $(LIB)) -lradial_cuda -Xlinker -rpath,'$$ORIGIN'
+
 oracle:
 	$(MAKE) -C oracle
 
 clean:
-	rm -rf build $(LIB)
+	rm -rf build $(LIB) $(DEBUG_LIB)
 	$(MAKE) -C oracle clean
 
-.PHONY: all lib oracle clean
+.PHONY: all lib debug oracle clean
 
 # kernel-variant libraries for tuning sweeps: make variant V=poly2 DEFS="-DRADIAL_POLY_PAIRS=2"
 variant:

@@ -121,7 +121,7 @@ inline Matrix masked_attention(const AttentionInstance& inst, const BlockLayout&
     const std::size_t n = inst.shape.total_tokens();
     auto q = detail::pack(inst.query), k = detail::pack(inst.key), v = detail::pack(inst.value);
     std::vector<std::uint16_t> o(q.size());
-    auto dev = upload(layout);
+    auto dev = upload_cached(layout);  // per-device cache: one upload for all heads of a call
     detail::check_status(radial_cuda_attn_fwd_host(q.data(), k.data(), v.data(), o.data(), nullptr, 1, n,
                                                    inst.head_dim, 0.f, dev.h, nullptr));
     Matrix out(n, inst.head_dim);
@@ -130,17 +130,16 @@ inline Matrix masked_attention(const AttentionInstance& inst, const BlockLayout&
 }
 
 // radial::masked_attention(inst, PatternSpec) (attention.hpp:184-225): the token-exact
-// mask on the B200 (K2 in token mode over the pattern's 128-block layout).  Frame-structured
-// kinds only (power: invalid_argument on the device path).
+// mask on the B200 (K2 in token mode over the pattern's 128-block layout), every kind.
 inline Matrix masked_attention(const AttentionInstance& inst, const PatternSpec& pattern) {
     detail::check_device_instance(inst);
     pattern.validate();
     const std::size_t n = inst.shape.total_tokens();
     radial_layout* h = nullptr;
-    detail::check_status(radial_cuda_mask_build(inst.shape.frames, inst.shape.tokens_per_frame, 128,
-                                                static_cast<int>(pattern.kind), pattern.sink ? 1 : 0,
-                                                pattern.temporal_window.value_or(0),
-                                                pattern.spatial_window.value_or(0), nullptr, &h));
+    detail::check_status(radial_cuda_layout_acquire(inst.shape.frames, inst.shape.tokens_per_frame, 128,
+                                                    static_cast<int>(pattern.kind), pattern.sink ? 1 : 0,
+                                                    pattern.temporal_window.value_or(RADIAL_WINDOW_NONE),
+                                                    pattern.spatial_window.value_or(RADIAL_WINDOW_NONE), nullptr, &h));
     detail::DeviceLayout dev(h);
     auto q = detail::pack(inst.query), k = detail::pack(inst.key), v = detail::pack(inst.value);
     std::vector<std::uint16_t> o(q.size());

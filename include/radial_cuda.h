@@ -30,7 +30,7 @@
 extern "C" {
 #endif
 
-#define RADIAL_CUDA_ABI_VERSION 1
+#define RADIAL_CUDA_ABI_VERSION 2
 
 enum radial_status {
     RADIAL_OK = 0,
@@ -52,6 +52,12 @@ enum radial_kind {
     RADIAL_KIND_HARMONIC = 6
 };
 
+/* "window absent" (PatternSpec's empty std::optional, grid.hpp:83-139): a kind that reads a
+ * window it was not given fails with RADIAL_ERR_INVALID "<kind> pattern requires
+ * temporal_window" / "... spatial_window", as PatternSpec::validate throws.  Kinds that do
+ * not read a window ignore the argument. */
+#define RADIAL_WINDOW_NONE 0xFFFFFFFFu
+
 typedef struct radial_layout radial_layout; /* opaque device-resident block layout */
 
 typedef struct radial_layout_info {
@@ -69,16 +75,32 @@ const char* radial_cuda_last_error(void);
  *      (block.hpp:59-120, keep rule mask.hpp:105-154).  Builds the CSR
  *      (bit-exact with the reference), its transpose and the kernel work lists
  *      on the device.  temporal_window / spatial_window are read only by the
- *      kinds that need them (grid.hpp:83-139). */
+ *      kinds that need them (grid.hpp:83-139); pass RADIAL_WINDOW_NONE when absent. */
 int radial_cuda_mask_build(uint32_t frames, uint32_t tokens_per_frame, uint32_t block_size,
                            int kind, int sink, uint32_t temporal_window,
                            uint32_t spatial_window, void* stream, radial_layout** out);
 
 /* Uploads a host CSR (e.g. from radial::deserialize, block.hpp:239-307) and
- * builds the device work lists for it.  Validates the CSR like deserialize. */
+ * builds the device work lists for it.  Validates the CSR like deserialize (which
+ * accepts row_ptr[0] != 0: the entries before it belong to no row; the uploaded layout
+ * drops them, so its kept_blocks / copy_csr count only the rows' entries). */
 int radial_cuda_layout_from_csr(uint32_t frames, uint32_t tokens_per_frame, uint32_t block_size,
                                 int kind, int sink, uint32_t grid_rows, const uint64_t* row_ptr,
                                 const uint32_t* col_idx, void* stream, radial_layout** out);
+
+/* ---- per-device layout cache (reference callers pass the same layout once per head,
+ *      attention.hpp:229): like radial_cuda_mask_build / radial_cuda_layout_from_csr, but
+ *      the handle is shared with a cache keyed by (device, shape, block size, pattern) --
+ *      for a CSR also by its contents -- so repeated calls skip the upload and the work-list
+ *      build.  Release the handle with radial_cuda_layout_free as usual (it drops one
+ *      reference).  The cache keeps up to 16 layouts (least recently used evicted). */
+int radial_cuda_layout_acquire(uint32_t frames, uint32_t tokens_per_frame, uint32_t block_size,
+                               int kind, int sink, uint32_t temporal_window, uint32_t spatial_window,
+                               void* stream, radial_layout** out);
+int radial_cuda_layout_acquire_csr(uint32_t frames, uint32_t tokens_per_frame, uint32_t block_size,
+                                   int kind, int sink, uint32_t grid_rows, const uint64_t* row_ptr,
+                                   const uint32_t* col_idx, void* stream, radial_layout** out);
+void radial_cuda_layout_cache_clear(void);
 
 int radial_cuda_layout_info(const radial_layout* layout, radial_layout_info* info);
 
@@ -94,7 +116,15 @@ int radial_cuda_layout_copy_csc(const radial_layout* layout, uint64_t* col_ptr, 
 int radial_cuda_layout_device_csr(const radial_layout* layout, const uint64_t** row_ptr,
                                   const uint32_t** col_idx);
 
+/* Drops one reference; the last one frees the device buffers stream-ordered after the
+ * work already queued on them (every stream that launched a kernel reading the layout),
+ * without synchronising the device.  A layout used inside a captured CUDA graph must
+ * outlive the graph. */
 void radial_cuda_layout_free(radial_layout* layout);
+
+/* Kernels this library has launched in this process (all entry points, mask builder
+ * included) -- the count a benchmark reports for its timed region. */
+uint64_t radial_cuda_kernel_launches(void);
 
 /* ---- sparse forward: replaces radial::masked_attention(const AttentionInstance&,
  *      const BlockLayout&) (attention.hpp:229-270) for all heads at once.
@@ -119,7 +149,8 @@ int radial_cuda_attn_fwd_scatter(const void* q, const void* k, const void* v, vo
 /* ---- token-exact forward: replaces radial::masked_attention(const AttentionInstance&,
  *      const PatternSpec&) (attention.hpp:184-225).  Iterates the blocks of a layout built
  *      by radial_cuda_mask_build (a superset, block.hpp:59) and keeps exactly the token
- *      pairs of the pattern's rule (mask.hpp:105-154, 238-272).  Frame-structured kinds only. */
+ *      pairs of the pattern's rule (mask.hpp:105-154, 238-272), every kind (power: the token
+ *      distance rule of mask.hpp:246-270). */
 int radial_cuda_attn_fwd_token(const void* q, const void* k, const void* v, void* o, float* lse,
                                uint32_t heads, uint64_t n, uint32_t head_dim, float scale,
                                const radial_layout* layout, void* stream);

@@ -53,6 +53,11 @@ def library_path() -> str:
     return _LIB_PATH
 
 
+def debug_library_path() -> str:
+    """Diagnostics library (tcgen05 / pipe microbenchmarks for scripts/; not the product path)."""
+    return os.path.join(os.path.dirname(_LIB_PATH), "libradial_debug.so")
+
+
 if not os.path.exists(_LIB_PATH):
     raise ImportError(
         f"paper_2506_19852_b200: CUDA library {_LIB_PATH} is missing; build it with "
@@ -87,6 +92,9 @@ _sig("radial_cuda_layout_copy_csr", _i32, _vp, _vp, _vp)
 _sig("radial_cuda_layout_copy_csc", _i32, _vp, _vp, _vp)
 _sig("radial_cuda_layout_device_csr", _i32, _vp, C.POINTER(_vp), C.POINTER(_vp))
 _sig("radial_cuda_layout_free", None, _vp)
+_sig("radial_cuda_layout_acquire", _i32, _u32, _u32, _u32, _i32, _i32, _u32, _u32, _vp, C.POINTER(_vp))
+_sig("radial_cuda_layout_cache_clear", None)
+_sig("radial_cuda_kernel_launches", _u64)
 _sig("radial_cuda_attn_fwd", _i32, _vp, _vp, _vp, _vp, _vp, _u32, _u64, _u32, _f32, _vp, _vp)
 _sig("radial_cuda_attn_fwd_token", _i32, _vp, _vp, _vp, _vp, _vp, _u32, _u64, _u32, _f32, _vp, _vp)
 _sig("radial_cuda_attn_fwd_host_multi", _i32, _vp, _vp, _vp, _vp, _vp, _u32, _u64, _u32, _f32, _u32, _u32, _u32,
@@ -103,6 +111,19 @@ _sig("radial_cuda_attention_flops", _i32, _vp, _u32, _u32, C.POINTER(_f64), C.PO
 _sig("radial_cuda_sparsity", _f64, _vp)
 
 RADIAL_OK, ERR_INVALID, ERR_EMPTY_ROW, ERR_CUDA, ERR_OOM, ERR_LENGTH = 0, 1, 2, 3, 4, 5
+WINDOW_NONE = 0xFFFFFFFF  # RADIAL_WINDOW_NONE: PatternSpec window absent
+# GEMMs the backward kernels issue per kept block, in units of the forward's two (QK^T, PV):
+# the dQ kernel computes S, dP, dQ and the dK/dV kernel S, dP, dV, dK -> 7 / 2
+BWD_EXECUTED_FACTOR = 3.5
+
+
+def kernel_launches() -> int:
+    """CUDA kernels this library has launched in this process (radial_cuda_kernel_launches)."""
+    return int(_lib.radial_cuda_kernel_launches())
+
+
+def _window(w) -> int:
+    return WINDOW_NONE if w is None else int(w)
 
 
 class LengthError(ValueError):
@@ -314,8 +335,8 @@ def device_layout(shape: GridShape, pattern: PatternSpec, block_size: int, *, ca
             return hit
     h = C.c_void_p()
     _check(_lib.radial_cuda_mask_build(shape.frames, shape.tokens_per_frame, block_size,
-                                       pattern.kind, int(pattern.sink), pattern.temporal_window or 0,
-                                       pattern.spatial_window or 0, _stream_ptr(stream), C.byref(h)))
+                                       pattern.kind, int(pattern.sink), _window(pattern.temporal_window),
+                                       _window(pattern.spatial_window), _stream_ptr(stream), C.byref(h)))
     lay = DeviceLayout(h.value, shape, block_size, pattern.kind, pattern.sink)
     if cache:
         with _cache_lock:
@@ -465,6 +486,21 @@ def _check_qkv(q, k, v):
     return q.shape
 
 
+def _check_out(o, lse, q, who: str):
+    """Caller-provided outputs must match what the kernel writes: O bf16 contiguous with q's
+    shape and device, lse fp32 contiguous [heads, n] on the same device."""
+    import torch
+    H, n, _ = q.shape
+    if o is not None:
+        if (not isinstance(o, torch.Tensor) or o.dtype != torch.bfloat16 or tuple(o.shape) != tuple(q.shape)
+                or o.device != q.device or not o.is_contiguous()):
+            raise ValueError(f"{who}: out must be a contiguous bfloat16 tensor of shape {tuple(q.shape)} on {q.device}")
+    if lse is not None:
+        if (not isinstance(lse, torch.Tensor) or lse.dtype != torch.float32 or tuple(lse.shape) != (H, n)
+                or lse.device != q.device or not lse.is_contiguous()):
+            raise ValueError(f"{who}: lse must be a contiguous float32 tensor of shape {(H, n)} on {q.device}")
+
+
 def _as_device_layout(layout) -> DeviceLayout:
     if isinstance(layout, DeviceLayout):
         return layout
@@ -484,6 +520,7 @@ def masked_attention(q, k, v, layout, scale: Optional[float] = None, *, out=None
     L = _as_device_layout(layout)
     if L.shape.total_tokens() != n:
         raise ValueError("masked_attention: layout shape mismatch")
+    _check_out(out, lse, q, "masked_attention")
     o = out if out is not None else torch.empty_like(q)
     if return_lse and lse is None:
         lse = torch.empty((H, n), dtype=torch.float32, device=q.device)
@@ -503,6 +540,7 @@ def masked_attention_scatter(q, k, v, layout, dst_ptrs, head_base: int, heads_fu
     L = _as_device_layout(layout)
     if L.shape.total_tokens() != n:
         raise ValueError("masked_attention: layout shape mismatch")
+    _check_out(None, lse, q, "masked_attention_scatter")
     ptrs = (_vp * len(dst_ptrs))(*[int(x) for x in dst_ptrs])
     _check(_lib.radial_cuda_attn_fwd_scatter(q.data_ptr(), k.data_ptr(), v.data_ptr(), ptrs, len(dst_ptrs),
                                              head_base, heads_full,
@@ -521,6 +559,7 @@ def masked_attention_pattern(q, k, v, shape: GridShape, pattern: PatternSpec, sc
     if shape.total_tokens() != n:
         raise ValueError("masked_attention: layout shape mismatch")
     L = device_layout(shape, pattern, block_size, stream=stream)
+    _check_out(out, lse, q, "masked_attention")
     o = out if out is not None else torch.empty_like(q)
     if return_lse and lse is None:
         lse = torch.empty((H, n), dtype=torch.float32, device=q.device)
@@ -535,6 +574,7 @@ def dense_attention(q, k, v, scale: Optional[float] = None, *, block_size: int =
     """radial::dense_attention (attention.hpp:141-163): the dense comparator kernel (K4)."""
     import torch
     H, n, d = _check_qkv(q, k, v)
+    _check_out(out, lse, q, "dense_attention")
     o = out if out is not None else torch.empty_like(q)
     if return_lse and lse is None:
         lse = torch.empty((H, n), dtype=torch.float32, device=q.device)
@@ -553,10 +593,17 @@ def masked_attention_host(q: np.ndarray, k: np.ndarray, v: np.ndarray, layout,
         if a.dtype != np.uint16 or a.ndim != 3 or not a.flags.c_contiguous:
             raise ValueError(f"masked_attention_host: {name} must be contiguous uint16 (bf16 bits)"
                              " [heads, n, head_dim]")
+    if not (q.shape == k.shape == v.shape):
+        raise ValueError("masked_attention_host: Q, K and V must have the same shape")
     H, n, d = q.shape
     L = _as_device_layout(layout)
     if o is None:
         o = np.empty_like(q)
+    elif o.dtype != np.uint16 or o.shape != q.shape or not o.flags.c_contiguous or not o.flags.writeable:
+        raise ValueError(f"masked_attention_host: o must be a writeable contiguous uint16 array of shape {q.shape}")
+    if lse is not None and (lse.dtype != np.float32 or lse.shape != (H, n) or not lse.flags.c_contiguous
+                            or not lse.flags.writeable):
+        raise ValueError(f"masked_attention_host: lse must be a writeable contiguous float32 array of shape {(H, n)}")
     _check(_lib.radial_cuda_attn_fwd_host(q.ctypes.data, k.ctypes.data, v.ctypes.data, o.ctypes.data,
                                           lse.ctypes.data if lse is not None else None, H, n, d,
                                           float(scale or 0.0), L.handle, None))
@@ -568,6 +615,11 @@ def masked_attention_backward(q, k, v, o, lse, dout, layout, scale: Optional[flo
     """Gradients (dq, dk, dv) of :func:`masked_attention` over the same layout (K3)."""
     import torch
     H, n, d = _check_qkv(q, k, v)
+    if o is None or lse is None or dout is None:
+        raise ValueError("masked_attention_backward: o, lse (the forward's return_lse=True outputs) and dout "
+                         "are required")
+    _check_out(o, lse, q, "masked_attention_backward")
+    _check_out(dout, None, q, "masked_attention_backward (dout)")
     L = _as_device_layout(layout)
     dq = torch.empty_like(q)
     dk = torch.empty_like(k)

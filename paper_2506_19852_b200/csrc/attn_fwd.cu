@@ -134,7 +134,9 @@ struct FwdCfg {
     static constexpr int kSmemAlloc = kSmemBytes + 1024;  // slack for 1024 B alignment
     // TMEM columns
     static constexpr uint32_t kColS0 = 0, kColS1 = BK, kColO0 = 2 * BK, kColO1 = 2 * BK + D;
-    static constexpr uint32_t kTmemCols = (2 * BK + 2 * D) <= 256 ? 256 : 512;
+    // always all 512 columns: the only possible allocation base is then column 0, which the
+    // MMA operands assume (a smaller request could be placed above another kernel's columns)
+    static constexpr uint32_t kTmemCols = 512;
     static constexpr uint32_t kIdescS = idesc_bf16(128, BK, 0, 0);
     static constexpr uint32_t kIdescO = idesc_bf16(128, D, 0, 1);
 };
@@ -209,9 +211,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
-    // The CTA owns all TMEM columns of its SM (one CTA per SM), so the allocation
-    // starts at lane 0 / column 0; the constant base keeps tcgen05 operands uniform.
-    if (*tmem_slot != 0) __trap();
+    // The CTA allocates all 512 TMEM columns of its SM, so the allocation starts at lane 0 /
+    // column 0 by construction; the constant base keeps tcgen05 operands uniform.
     constexpr uint32_t tmem = kTmem;
     // producer / MMA / allocator warpgroup needs few registers (the grouped MMA issue keeps
     // its operands in uniform registers); the two softmax warpgroups hold a 128-column S row
@@ -504,7 +505,34 @@ __global__ void __launch_bounds__(kThreads, 1)
                 // (i, k) in each key frame j the block overlaps (mask.hpp:238-272)
 #pragma unroll
                 for (int w = 0; w < BK / 32; ++w) kmask[w] = 0u;
-                if (active && grow < p.n) {
+                if (active && grow < p.n && p.rule.kind == RADIAL_KIND_POWER) {
+                    // power rule (mask.hpp:246-270): key v is kept iff |u - v| is 0 or a power of
+                    // two, or (sink) v lies in frame 0
+                    const uint64_t v0 = static_cast<uint64_t>(J) * BK, vn = static_cast<uint64_t>(valid);
+                    auto set = [&](uint64_t v) {
+                        if (v < v0 || v - v0 >= vn) return;
+                        const uint32_t c = static_cast<uint32_t>(v - v0);
+#pragma unroll
+                        for (int w = 0; w < BK / 32; ++w)
+                            if ((c >> 5) == static_cast<uint32_t>(w)) kmask[w] |= 1u << (c & 31);
+                    };
+                    if (p.rule.sink && v0 < p.rule.s) {
+                        const uint32_t hi = static_cast<uint32_t>(min(static_cast<uint64_t>(p.rule.s) - v0, vn));
+#pragma unroll
+                        for (int w = 0; w < BK / 32; ++w) {
+                            const int lw = 32 * w, hw = min(static_cast<int>(hi) - 1, 32 * w + 31);
+                            if (lw <= hw) {
+                                const int len = hw - lw + 1;
+                                kmask[w] |= len == 32 ? 0xffffffffu : ((1u << len) - 1u);
+                            }
+                        }
+                    }
+                    set(grow);
+                    for (uint64_t t = 1; t < p.n; t <<= 1) {
+                        if (grow >= t) set(grow - t);
+                        if (grow + t < p.n) set(grow + t);
+                    }
+                } else if (active && grow < p.n) {
                     const uint32_t v0 = J * BK, v1 = v0 + static_cast<uint32_t>(valid) - 1;
                     // key frame of the block's first key, tracked incrementally (the KV list is
                     // ascending) instead of a division per block
@@ -767,6 +795,8 @@ int launch_fwd_t(const void* q, const void* k, const void* v, void* o, float* ls
     if (items > 0x7fffffffull) return fail(RADIAL_ERR_INVALID, "too many work items");
     kern<<<static_cast<unsigned>(items), kThreads, Cfg::kSmemAlloc, st>>>(tq, tk, tv, p);
     RADIAL_CUDA_TRY(cudaGetLastError());
+    count_launches(1);
+    note_use(L, st);
     return RADIAL_OK;
 }
 

@@ -15,7 +15,7 @@
 //   CSR   rows = query blocks, cols = KV blocks     (BlockLayout)
 //   CSC   rows = KV blocks,    cols = query blocks  (backward dK/dV)
 //   chunk unions: rows = 256-token chunks, value = J | mask << 28
-//         (the forward / backward work lists).
+//         (the forward work lists).
 #include <algorithm>
 #include <numeric>
 #include <vector>
@@ -257,36 +257,88 @@ __global__ void __launch_bounds__(1024) lpt_sort_kernel(const uint64_t* __restri
     for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) order[i] = static_cast<uint32_t>(key[i] & 0xffffffffu);
 }
 
-// Forward chunk lists: each entry kept by tile 0 only is followed by the next entry kept by
-// tile 1 only (pulled forward from later in the list), so the forward's MMA warp can issue
-// that entry's S together with the first and the two solo steps overlap like one shared
-// step.  Everything else stays in ascending J order (K/V locality in L2).  One thread per
-// chunk; `in` is a copy of the fill order.
+// Forward chunk lists: each entry kept by tile 0 only ("open") is followed by a later entry
+// kept by tile 1 only ("close"), pulled forward, so the forward's MMA warp can issue that
+// entry's S together with the first and the two solo steps overlap like one shared step.
+// Everything else stays in ascending J order (K/V locality in L2).  The pairing is greedy
+// and first-in first-out: the m-th open takes the first close after it and after the
+// (m-1)-th open's partner.  That is bracket matching, so one warp per chunk decides it with
+// prefix counts: a close is matched iff it does not raise the running maximum of
+// (closes - opens) over the list prefix, and the m-th matched close belongs to the m-th
+// open.  Pass 1 records the matched closes' positions (in `scratch`, at the chunk's list
+// offset), pass 2 scatters every entry to its output slot.  `in` is the fill order.
 __global__ void __launch_bounds__(256) pair_solo_entries(const uint64_t* __restrict__ ptr, uint32_t C, uint32_t GT,
-                                                         const uint32_t* __restrict__ in, uint32_t* __restrict__ out) {
-    const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
-    if (c >= C) return;
+                                                         const uint32_t* __restrict__ in, uint32_t* __restrict__ out,
+                                                         uint32_t* __restrict__ scratch) {
+    const uint32_t c = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint32_t lane = threadIdx.x & 31;
+    if (c >= C) return;  // whole warps exit together
     const uint64_t b = ptr[c], e = ptr[c + 1];
     const uint32_t m0 = (1u << GT) - 1u;
-    auto kind = [&](uint32_t x) {  // 0 shared, 1 tile-0 only, 2 tile-1 only
+    const uint32_t below = (1u << lane) - 1u;
+    auto kind = [&](uint32_t x) {  // 0 shared, 1 tile-0 only (open), 2 tile-1 only (close)
         const uint32_t m = x >> 28;
         const bool a = m & m0, bb = (m >> GT) & m0;
         return (a && bb) ? 0 : (a ? 1 : 2);
     };
-    uint64_t o = b, nb = b;  // nb: one past the last tile-1-only entry pulled forward
-    for (uint64_t i = b; i < e; ++i) {
-        const uint32_t x = in[i];
-        const int k = kind(x);
-        if (k == 2 && i < nb) continue;  // already emitted behind a tile-0-only entry
-        out[o++] = x;
-        if (k == 1) {
-            uint64_t q = nb > i + 1 ? nb : i + 1;
-            while (q < e && kind(in[q]) != 2) ++q;
-            if (q < e) {
-                out[o++] = in[q];
-                nb = q + 1;
-            }
+    // one 32-entry tile: kind of this lane's entry and whether it is a matched close; carries
+    // opens / closes seen and the running max excess U across tiles
+    struct Carry {
+        uint32_t opens = 0, closes = 0;
+        int U = 0;
+    };
+    auto tile = [&](uint64_t i, Carry& cy, int& k, bool& matched, uint32_t& bo) {
+        k = i < e ? kind(in[i]) : 0;
+        bo = __ballot_sync(0xffffffffu, k == 1);
+        const uint32_t bc = __ballot_sync(0xffffffffu, k == 2);
+        const uint32_t upto = below | (1u << lane);
+        int x = static_cast<int>(cy.closes + __popc(bc & upto)) - static_cast<int>(cy.opens + __popc(bo & upto));
+        for (int o = 1; o < 32; o <<= 1) {  // inclusive prefix max over the lanes
+            const int y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= static_cast<uint32_t>(o)) x = max(x, y);
         }
+        const int prev = __shfl_up_sync(0xffffffffu, x, 1);
+        const int u_before = lane ? max(cy.U, prev) : cy.U;
+        const int u_after = max(cy.U, x);
+        matched = k == 2 && u_after == u_before;
+        cy.U = __shfl_sync(0xffffffffu, u_after, 31);
+        cy.opens += __popc(bo);
+        cy.closes += __popc(bc);
+    };
+    Carry cy;
+    uint32_t nm = 0;  // matched closes so far
+    for (uint64_t base = b; base < e; base += 32) {
+        int k;
+        bool matched;
+        uint32_t bo;
+        tile(base + lane, cy, k, matched, bo);
+        const uint32_t bm = __ballot_sync(0xffffffffu, matched);
+        if (matched) scratch[b + nm + __popc(bm & below)] = static_cast<uint32_t>(base + lane);
+        nm += __popc(bm);
+    }
+    Carry cy2;
+    uint64_t opos = b;
+    for (uint64_t base = b; base < e; base += 32) {
+        const uint64_t i = base + lane;
+        int k;
+        bool matched;
+        uint32_t bo;
+        const uint32_t opens_before = cy2.opens;
+        tile(i, cy2, k, matched, bo);
+        const uint32_t om = opens_before + __popc(bo & below);  // index of this open
+        const bool pair = k == 1 && om < nm;
+        const uint32_t contrib = (i >= e || matched) ? 0u : (pair ? 2u : 1u);
+        uint32_t x = contrib;  // inclusive prefix sum
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= static_cast<uint32_t>(o)) x += y;
+        }
+        const uint64_t pos = opos + x - contrib;
+        if (contrib) {
+            out[pos] = in[i];
+            if (pair) out[pos + 1] = in[scratch[b + om]];
+        }
+        opos += __shfl_sync(0xffffffffu, x, 31);
     }
 }
 
@@ -297,6 +349,7 @@ int count_and_scan(F pred, uint32_t rows, uint32_t cols, uint32_t* counts, uint6
     if (rows) list_count<F><<<rows, kThreads, 0, st>>>(pred, cols, counts);
     scan_rows<<<1, 1024, 0, st>>>(counts, rows, ptr, dstats);
     RADIAL_CUDA_TRY(cudaGetLastError());
+    radial_detail::count_launches(rows ? 2 : 1);
     return RADIAL_OK;
 }
 
@@ -305,6 +358,7 @@ int fill(F pred, uint32_t rows, uint32_t cols, const uint64_t* ptr, uint32_t* id
          cudaStream_t st) {
     if (rows) list_fill<F><<<rows, kThreads, 0, st>>>(pred, cols, ptr, idx, with_mask);
     RADIAL_CUDA_TRY(cudaGetLastError());
+    if (rows) radial_detail::count_launches(1);
     return RADIAL_OK;
 }
 
@@ -320,6 +374,7 @@ int lpt_order(const uint64_t* dptr, uint32_t n, cudaStream_t st, uint32_t** orde
     if (n <= static_cast<uint32_t>(kSortMax)) {
         lpt_sort_kernel<<<1, 1024, 0, st>>>(dptr, n, window, *order_out);
         RADIAL_CUDA_TRY(cudaGetLastError());
+        radial_detail::count_launches(1);
         return RADIAL_OK;
     }
     std::vector<uint64_t> h(n + 1);
@@ -340,8 +395,8 @@ int lpt_order(const uint64_t* dptr, uint32_t n, cudaStream_t st, uint32_t** orde
 struct Scratch {
     cudaStream_t st;
     uint32_t* counts = nullptr;
-    ScanStats* stats = nullptr;  // [4] CSR, CSC, query-chunk unions, KV-chunk unions
-    ScanStats host[4];
+    ScanStats* stats = nullptr;  // [3] CSR, CSC, query-chunk unions
+    ScanStats host[3];
     explicit Scratch(cudaStream_t s) : st(s) {}
     ~Scratch() {
         if (counts) cudaFreeAsync(counts, st);
@@ -381,8 +436,8 @@ int build_worklists(radial_layout* L, cudaStream_t st) {
     L->G = attn ? 256 / L->B : 1;
     L->C = attn ? (R + L->G - 1) / L->G : 0;
     const uint32_t C = L->C;
-    RADIAL_CUDA_TRY(cudaMallocAsync(&sc.counts, sizeof(uint32_t) * (std::max<uint32_t>(R, 1) + 2 * std::max<uint32_t>(C, 1)), st));
-    RADIAL_CUDA_TRY(cudaMallocAsync(&sc.stats, 4 * sizeof(ScanStats), st));
+    RADIAL_CUDA_TRY(cudaMallocAsync(&sc.counts, sizeof(uint32_t) * (std::max<uint32_t>(R, 1) + std::max<uint32_t>(C, 1)), st));
+    RADIAL_CUDA_TRY(cudaMallocAsync(&sc.stats, 3 * sizeof(ScanStats), st));
     RADIAL_CUDA_TRY(cudaMallocAsync(&L->col_ptr, sizeof(uint64_t) * (static_cast<size_t>(R) + 1), st));
     RADIAL_CUDA_TRY(cudaMallocAsync(&L->row_idx, sizeof(uint32_t) * std::max<uint64_t>(L->nnz, 1), st));
     int rc;
@@ -395,30 +450,30 @@ int build_worklists(radial_layout* L, cudaStream_t st) {
         return RADIAL_OK;  // attention kernels not instantiated for this block size
     }
     RADIAL_CUDA_TRY(cudaMallocAsync(&L->uptr, sizeof(uint64_t) * (static_cast<size_t>(C) + 1), st));
-    RADIAL_CUDA_TRY(cudaMallocAsync(&L->tptr, sizeof(uint64_t) * (static_cast<size_t>(C) + 1), st));
     const ChunkUnion uq{L->row_ptr, L->col_idx, R, L->G};
-    const ChunkUnion ukv{L->col_ptr, L->row_idx, R, L->G};
     if ((rc = count_and_scan(uq, C, R, sc.counts + R, L->uptr, sc.stats + 2, st))) return rc;
-    if ((rc = count_and_scan(ukv, C, R, sc.counts + R + C, L->tptr, sc.stats + 3, st))) return rc;
     if ((rc = lpt_order(L->row_ptr, R, st, &L->rorder))) return rc;
     if ((rc = lpt_order(L->col_ptr, R, st, &L->corder))) return rc;
     if ((rc = lpt_order(L->uptr, C, st, &L->uorder))) return rc;
-    if ((rc = lpt_order(L->tptr, C, st, &L->torder))) return rc;
-    RADIAL_CUDA_TRY(cudaMemcpyAsync(sc.host, sc.stats, 4 * sizeof(ScanStats), cudaMemcpyDeviceToHost, st));
+    RADIAL_CUDA_TRY(cudaMemcpyAsync(sc.host, sc.stats, 3 * sizeof(ScanStats), cudaMemcpyDeviceToHost, st));
     RADIAL_CUDA_TRY(cudaStreamSynchronize(st));
     if (sc.host[1].nnz != L->nnz) return fail(RADIAL_ERR_INVALID, "layout transpose size mismatch");
-    RADIAL_CUDA_TRY(cudaMallocAsync(&L->uidx, sizeof(uint32_t) * std::max<uint64_t>(sc.host[2].nnz, 1), st));
-    RADIAL_CUDA_TRY(cudaMallocAsync(&L->tidx, sizeof(uint32_t) * std::max<uint64_t>(sc.host[3].nnz, 1), st));
-    if ((rc = fill(uq, C, R, L->uptr, L->uidx, 1, st))) return rc;
-    if (C && sc.host[2].nnz) {
-        uint32_t* tmp = nullptr;
-        RADIAL_CUDA_TRY(cudaMallocAsync(&tmp, sizeof(uint32_t) * sc.host[2].nnz, st));
-        RADIAL_CUDA_TRY(cudaMemcpyAsync(tmp, L->uidx, sizeof(uint32_t) * sc.host[2].nnz, cudaMemcpyDeviceToDevice, st));
-        pair_solo_entries<<<(C + 255) / 256, 256, 0, st>>>(L->uptr, C, L->G / 2, tmp, L->uidx);
+    const uint64_t un = sc.host[2].nnz;
+    RADIAL_CUDA_TRY(cudaMallocAsync(&L->uidx, sizeof(uint32_t) * std::max<uint64_t>(un, 1), st));
+    RADIAL_CUDA_TRY(cudaMallocAsync(&L->uidx_asc, sizeof(uint32_t) * std::max<uint64_t>(un, 1), st));
+    // ascending lists (token-exact forward) filled directly, then the paired copy for the
+    // block-layout forward
+    if ((rc = fill(uq, C, R, L->uptr, L->uidx_asc, 1, st))) return rc;
+    if (C && un) {
+        uint32_t* match = nullptr;
+        RADIAL_CUDA_TRY(cudaMallocAsync(&match, sizeof(uint32_t) * un, st));
+        const uint32_t warps_per_cta = 8;
+        pair_solo_entries<<<(C + warps_per_cta - 1) / warps_per_cta, 32 * warps_per_cta, 0, st>>>(
+            L->uptr, C, L->G / 2, L->uidx_asc, L->uidx, match);
         RADIAL_CUDA_TRY(cudaGetLastError());
-        L->uidx_asc = tmp;  // kept for the token-exact forward (incremental key-frame tracking)
+        count_launches(1);
+        RADIAL_CUDA_TRY(cudaFreeAsync(match, st));
     }
-    if ((rc = fill(ukv, C, R, L->tptr, L->tidx, 1, st))) return rc;
     RADIAL_CUDA_TRY(cudaStreamSynchronize(st));
     return RADIAL_OK;
 }

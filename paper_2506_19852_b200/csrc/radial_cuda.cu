@@ -1,5 +1,6 @@
 // radial_cuda.cu -- the C-ABI (include/radial_cuda.h): layout handles,
 // argument validation with the reference's error semantics, launches.
+#include <atomic>
 #include <cstring>
 #include <new>
 #include <mutex>
@@ -13,6 +14,32 @@
 namespace radial_detail {
 
 thread_local std::string g_last_error;
+std::atomic<uint64_t> g_launches{0};
+
+void count_launches(uint64_t k) { g_launches.fetch_add(k, std::memory_order_relaxed); }
+
+void note_use(const radial_layout* Lc, cudaStream_t st) {
+    if (!Lc) return;
+    auto* L = const_cast<radial_layout*>(Lc);
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) {
+        cudaGetLastError();
+        return;
+    }
+    std::lock_guard<std::mutex> g(L->use_mu);
+    for (auto& u : L->uses)
+        if (u.first == st) {
+            // a destroyed stream's handle can be reused by a new one: order the new stream after
+            // the old event before replacing it, so no earlier use is lost (no-op on one stream)
+            cudaStreamWaitEvent(st, u.second, 0);
+            cudaEventRecord(u.second, st);
+            return;
+        }
+    cudaEvent_t e;
+    if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return;
+    cudaEventRecord(e, st);
+    L->uses.emplace_back(st, e);
+}
 
 void set_error(const std::string& msg) { g_last_error = msg; }
 int fail(int code, const std::string& msg) {
@@ -39,17 +66,53 @@ using namespace radial_detail;
 
 namespace {
 
+// Per-device stream on which layouts are freed (stream-ordered, after their last uses).
+cudaStream_t free_stream(int dev) {
+    static std::mutex mu;
+    static cudaStream_t streams[64] = {};
+    if (dev < 0 || dev >= 64) return nullptr;
+    std::lock_guard<std::mutex> g(mu);
+    if (!streams[dev] && cudaStreamCreateWithFlags(&streams[dev], cudaStreamNonBlocking) != cudaSuccess) {
+        cudaGetLastError();
+        streams[dev] = nullptr;
+    }
+    return streams[dev];
+}
+
+// Drops one reference; the last one frees the device buffers stream-ordered: a private
+// stream waits for the layout's recorded uses (one event per stream that launched work on
+// it) and releases the buffers with cudaFreeAsync -- no device-wide synchronisation, and
+// correct whichever device is current.
 void free_layout(radial_layout* L) {
     if (!L) return;
-    // stream-ordered (pool) allocations are not implicitly synchronised by cudaFree:
-    // drain any in-flight kernel that may still read the layout
-    cudaDeviceSynchronize();
-    void* ptrs[] = {L->row_ptr, L->col_idx, L->col_ptr, L->row_idx, L->uptr,   L->uidx,
-                    L->uorder,  L->tptr,    L->tidx,    L->torder,  L->rorder, L->corder,
-                    L->uidx_asc};
+    if (L->refs.fetch_sub(1, std::memory_order_acq_rel) != 1) return;
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (cur != L->device) cudaSetDevice(L->device);
+    cudaStream_t fs = free_stream(L->device);
+    {
+        std::lock_guard<std::mutex> g(L->use_mu);
+        for (auto& u : L->uses) {
+            if (fs) cudaStreamWaitEvent(fs, u.second, 0);
+            else cudaEventSynchronize(u.second);
+            cudaEventDestroy(u.second);
+        }
+        L->uses.clear();
+    }
+    void* ptrs[] = {L->row_ptr, L->col_idx, L->col_ptr, L->row_idx, L->uptr,
+                    L->uidx,    L->uorder,  L->rorder,  L->corder,  L->uidx_asc};
     for (void* p : ptrs)
-        if (p) cudaFree(p);
+        if (p) cudaFreeAsync(p, fs);
+    cudaGetLastError();  // teardown at process exit may find the context gone
+    if (cur >= 0 && cur != L->device) cudaSetDevice(cur);
     delete L;
+}
+
+// A failed build frees what it allocated after the work it queued on `st`.
+int bail_layout(radial_layout* L, cudaStream_t st, int rc) {
+    note_use(L, st);
+    free_layout(L);
+    return rc;
 }
 
 int check_shape(uint32_t f, uint32_t s, uint32_t B) {
@@ -63,12 +126,17 @@ int check_shape(uint32_t f, uint32_t s, uint32_t B) {
     return RADIAL_OK;
 }
 
-int check_pattern(int kind, uint32_t tw, uint32_t sw, bool has_tw, bool has_sw) {
+// PatternSpec::validate (grid.hpp:118-139): a kind that reads a window must be given one
+// (RADIAL_WINDOW_NONE = absent).
+int check_pattern(int kind, uint32_t tw, uint32_t sw) {
+    static const char* names[] = {"radial", "dense", "spatial", "temporal", "sta", "power", "harmonic"};
     if (kind < 0 || kind > RADIAL_KIND_HARMONIC) return fail(RADIAL_ERR_INVALID, "unknown pattern kind");
-    (void)tw;
-    (void)sw;
-    (void)has_tw;
-    (void)has_sw;
+    const bool reads_tw = kind == RADIAL_KIND_SPATIAL || kind == RADIAL_KIND_STA;
+    const bool reads_sw = kind == RADIAL_KIND_TEMPORAL || kind == RADIAL_KIND_STA;
+    if (reads_tw && tw == RADIAL_WINDOW_NONE)
+        return fail(RADIAL_ERR_INVALID, std::string(names[kind]) + " pattern requires temporal_window");
+    if (reads_sw && sw == RADIAL_WINDOW_NONE)
+        return fail(RADIAL_ERR_INVALID, std::string(names[kind]) + " pattern requires spatial_window");
     return RADIAL_OK;
 }
 
@@ -120,10 +188,11 @@ struct HostPipe {
     }
 };
 
-int host_fwd(const void* q, const void* k, const void* v, void* o, float* lse, uint32_t heads,
-             uint64_t n, uint32_t head_dim, uint32_t BK, float scale, const radial_layout* L,
-             cudaStream_t st, bool token = false) {
-    thread_local HostPipe hp;
+thread_local HostPipe t_hp;
+
+int host_fwd_impl(HostPipe& hp, const void* q, const void* k, const void* v, void* o, float* lse, uint32_t heads,
+                  uint64_t n, uint32_t head_dim, uint32_t BK, float scale, const radial_layout* L,
+                  cudaStream_t st, bool token) {
     int dev = 0;
     RADIAL_CUDA_TRY(cudaGetDevice(&dev));
     const size_t hbytes = static_cast<size_t>(n) * head_dim * 2;  // one head of one tensor
@@ -210,6 +279,23 @@ int host_fwd(const void* q, const void* k, const void* v, void* o, float* lse, u
     return RADIAL_OK;
 }
 
+// On a mid-pipeline failure the copies already queued still read the caller's q/k/v and write
+// o/lse: drain every pipeline stream before returning, so the caller may free its buffers.
+int host_fwd(const void* q, const void* k, const void* v, void* o, float* lse, uint32_t heads,
+             uint64_t n, uint32_t head_dim, uint32_t BK, float scale, const radial_layout* L,
+             cudaStream_t st, bool token = false) {
+    const int rc = host_fwd_impl(t_hp, q, k, v, o, lse, heads, n, head_dim, BK, scale, L, st, token);
+    if (rc != RADIAL_OK) {
+        const std::string msg = g_last_error;
+        for (cudaStream_t s : {t_hp.in, t_hp.out, t_hp.comp[0], t_hp.comp[1]})
+            if (s) cudaStreamSynchronize(s);
+        cudaStreamSynchronize(st);
+        cudaGetLastError();
+        g_last_error = msg;
+    }
+    return rc;
+}
+
 }  // namespace
 
 extern "C" {
@@ -224,9 +310,13 @@ int radial_cuda_mask_build(uint32_t frames, uint32_t tokens_per_frame, uint32_t 
     *out = nullptr;
     int rc = check_shape(frames, tokens_per_frame, block_size);
     if (rc) return rc;
-    if ((rc = check_pattern(kind, temporal_window, spatial_window, true, true))) return rc;
+    if ((rc = check_pattern(kind, temporal_window, spatial_window))) return rc;
     auto* L = new radial_layout();
-    RADIAL_CUDA_TRY(cudaGetDevice(&L->device));
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (cudaGetDevice(&L->device) != cudaSuccess) {
+        delete L;
+        return cuda_fail(cudaGetLastError(), "cudaGetDevice");
+    }
     L->f = frames;
     L->s = tokens_per_frame;
     L->B = block_size;
@@ -236,11 +326,7 @@ int radial_cuda_mask_build(uint32_t frames, uint32_t tokens_per_frame, uint32_t 
     L->tw = temporal_window;
     L->sw = spatial_window;
     L->from_pattern = 1;
-    cudaStream_t st = static_cast<cudaStream_t>(stream);
-    if ((rc = build_layout_device(L, st)) || (rc = build_worklists(L, st))) {
-        free_layout(L);
-        return rc;
-    }
+    if ((rc = build_layout_device(L, st)) || (rc = build_worklists(L, st))) return bail_layout(L, st, rc);
     *out = L;
     return RADIAL_OK;
 }
@@ -252,13 +338,13 @@ int radial_cuda_layout_from_csr(uint32_t frames, uint32_t tokens_per_frame, uint
     *out = nullptr;
     int rc = check_shape(frames, tokens_per_frame, block_size);
     if (rc) return rc;
-    if ((rc = check_pattern(kind, 0, 0, true, true))) return rc;
+    if (kind < 0 || kind > RADIAL_KIND_HARMONIC) return fail(RADIAL_ERR_INVALID, "unknown pattern kind");
     const uint64_t R = (static_cast<uint64_t>(frames) * tokens_per_frame + block_size - 1) / block_size;
     if (grid_rows != R)
         return fail(RADIAL_ERR_INVALID, "grid_rows: expected " + std::to_string(R) + " for this shape, got " +
                                             std::to_string(grid_rows));
-    // validation as in deserialize (block.hpp:274-302)
-    if (row_ptr[0] != 0) return fail(RADIAL_ERR_INVALID, "row_ptr: must start at 0");
+    // validation as in deserialize (block.hpp:274-302), which accepts a nonzero row_ptr[0]:
+    // entries before it belong to no row and the uploaded layout drops them
     uint32_t mx = 0, mn = 0xffffffffu;
     int64_t first_empty = -1;
     for (uint64_t I = 0; I < R; ++I) {
@@ -269,24 +355,30 @@ int radial_cuda_layout_from_csr(uint32_t frames, uint32_t tokens_per_frame, uint
         mn = std::min<uint32_t>(mn, static_cast<uint32_t>(std::min<uint64_t>(len, 0xffffffffu)));
         if (len == 0 && first_empty < 0) first_empty = static_cast<int64_t>(I);
     }
-    const uint64_t nnz = row_ptr[R];
-    if (nnz > R * R) return fail(RADIAL_ERR_INVALID, "row_ptr: kept-block count exceeds grid capacity");
-    if (nnz && !col_idx) return fail(RADIAL_ERR_INVALID, "null col_idx");
+    if (row_ptr[R] > R * R) return fail(RADIAL_ERR_INVALID, "row_ptr: kept-block count exceeds grid capacity");
+    if (row_ptr[R] && !col_idx) return fail(RADIAL_ERR_INVALID, "null col_idx");
+    for (uint64_t e = 0; e < row_ptr[R]; ++e)
+        if (col_idx[e] >= R)
+            return fail(RADIAL_ERR_INVALID, "col_idx: column " + std::to_string(col_idx[e]) +
+                                                " out of range at entry " + std::to_string(e));
     for (uint64_t I = 0; I < R; ++I)
-        for (uint64_t e = row_ptr[I]; e < row_ptr[I + 1]; ++e) {
-            if (col_idx[e] >= R)
-                return fail(RADIAL_ERR_INVALID, "col_idx: column " + std::to_string(col_idx[e]) +
-                                                    " out of range at entry " + std::to_string(e));
-            if (e > row_ptr[I] && col_idx[e] <= col_idx[e - 1])
+        for (uint64_t e = row_ptr[I] + 1; e < row_ptr[I + 1]; ++e)
+            if (col_idx[e] <= col_idx[e - 1])
                 return fail(RADIAL_ERR_INVALID, "col_idx: not strictly increasing in row " + std::to_string(I));
-        }
+    const uint64_t base = row_ptr[0], nnz = row_ptr[R] - base;
+    std::vector<uint64_t> rp_norm;
+    const uint64_t* rp = row_ptr;
+    if (base) {
+        rp_norm.assign(row_ptr, row_ptr + R + 1);
+        for (auto& x : rp_norm) x -= base;
+        rp = rp_norm.data();
+    }
     auto* L = new radial_layout();
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    auto bail = [&](int code) {
-        free_layout(L);
-        return code;
-    };
-    if (cudaGetDevice(&L->device) != cudaSuccess) return bail(cuda_fail(cudaGetLastError(), "cudaGetDevice"));
+    if (cudaGetDevice(&L->device) != cudaSuccess) {
+        delete L;
+        return cuda_fail(cudaGetLastError(), "cudaGetDevice");
+    }
     L->f = frames;
     L->s = tokens_per_frame;
     L->B = block_size;
@@ -298,17 +390,154 @@ int radial_cuda_layout_from_csr(uint32_t frames, uint32_t tokens_per_frame, uint
     L->max_row_len = R ? mx : 0;
     L->min_row_len = R ? mn : 0;
     cudaError_t e;
-    if ((e = cudaMalloc(&L->row_ptr, sizeof(uint64_t) * (R + 1))) != cudaSuccess) return bail(cuda_fail(e, "cudaMalloc"));
-    if ((e = cudaMalloc(&L->col_idx, sizeof(uint32_t) * std::max<uint64_t>(nnz, 1))) != cudaSuccess)
-        return bail(cuda_fail(e, "cudaMalloc"));
-    if ((e = cudaMemcpyAsync(L->row_ptr, row_ptr, sizeof(uint64_t) * (R + 1), cudaMemcpyHostToDevice, st)) != cudaSuccess)
-        return bail(cuda_fail(e, "cudaMemcpyAsync"));
-    if (nnz && (e = cudaMemcpyAsync(L->col_idx, col_idx, sizeof(uint32_t) * nnz, cudaMemcpyHostToDevice, st)) != cudaSuccess)
-        return bail(cuda_fail(e, "cudaMemcpyAsync"));
-    if ((rc = build_worklists(L, st))) return bail(rc);
+    if ((e = cudaMallocAsync(&L->row_ptr, sizeof(uint64_t) * (R + 1), st)) != cudaSuccess ||
+        (e = cudaMallocAsync(&L->col_idx, sizeof(uint32_t) * std::max<uint64_t>(nnz, 1), st)) != cudaSuccess)
+        return bail_layout(L, st, cuda_fail(e, "cudaMallocAsync"));
+    if ((e = cudaMemcpyAsync(L->row_ptr, rp, sizeof(uint64_t) * (R + 1), cudaMemcpyHostToDevice, st)) != cudaSuccess)
+        return bail_layout(L, st, cuda_fail(e, "cudaMemcpyAsync"));
+    if (nnz && (e = cudaMemcpyAsync(L->col_idx, col_idx + base, sizeof(uint32_t) * nnz, cudaMemcpyHostToDevice, st)) !=
+                   cudaSuccess)
+        return bail_layout(L, st, cuda_fail(e, "cudaMemcpyAsync"));
+    if ((rc = build_worklists(L, st))) return bail_layout(L, st, rc);
     *out = L;
     return RADIAL_OK;
 }
+
+// ---- device layout cache: reference callers pass the same layout once
+// per head, so uploads / builds are kept per device and handed out with shared ownership.
+namespace {
+struct CacheEntry {
+    int dev;
+    uint32_t f, s, B, tw, sw;
+    int kind, sink;
+    bool csr;  // uploaded CSR (content compared) vs pattern-built
+    std::vector<uint64_t> rp;
+    std::vector<uint32_t> ci;
+    radial_layout* L;
+    uint64_t tick;
+};
+std::mutex g_cache_mu;
+std::vector<CacheEntry> g_cache;
+uint64_t g_cache_tick = 0;
+constexpr size_t kCacheMax = 16;
+
+bool same_key(const CacheEntry& c, const CacheEntry& k) {
+    if (c.dev != k.dev || c.f != k.f || c.s != k.s || c.B != k.B || c.kind != k.kind || c.sink != k.sink ||
+        c.csr != k.csr)
+        return false;
+    if (!k.csr) return c.tw == k.tw && c.sw == k.sw;
+    return c.rp.size() == k.rp.size() && c.ci.size() == k.ci.size() &&
+           std::memcmp(c.rp.data(), k.rp.data(), c.rp.size() * 8) == 0 &&
+           (c.ci.empty() || std::memcmp(c.ci.data(), k.ci.data(), c.ci.size() * 4) == 0);
+}
+
+radial_layout* cache_find(const CacheEntry& key) {
+    std::lock_guard<std::mutex> g(g_cache_mu);
+    for (auto& c : g_cache)
+        if (same_key(c, key)) {
+            c.tick = ++g_cache_tick;
+            c.L->refs.fetch_add(1, std::memory_order_acq_rel);
+            return c.L;
+        }
+    return nullptr;
+}
+
+// Inserts a freshly built layout (its one reference becomes the cache's) and returns it with
+// an extra reference for the caller; a concurrent insert of the same key wins.
+radial_layout* cache_insert(CacheEntry&& key, radial_layout* L) {
+    std::vector<radial_layout*> drop;
+    radial_layout* ret = nullptr;
+    {
+        std::lock_guard<std::mutex> g(g_cache_mu);
+        for (auto& c : g_cache)
+            if (same_key(c, key)) {
+                ret = c.L;
+                drop.push_back(L);
+                break;
+            }
+        if (!ret) {
+            key.L = L;
+            key.tick = ++g_cache_tick;
+            g_cache.push_back(std::move(key));
+            ret = L;
+            if (g_cache.size() > kCacheMax) {
+                auto old = std::min_element(g_cache.begin(), g_cache.end(),
+                                            [](const CacheEntry& a, const CacheEntry& b) { return a.tick < b.tick; });
+                drop.push_back(old->L);
+                g_cache.erase(old);
+            }
+        }
+        ret->refs.fetch_add(1, std::memory_order_acq_rel);
+    }
+    for (auto* d : drop) free_layout(d);
+    return ret;
+}
+}  // namespace
+
+int radial_cuda_layout_acquire(uint32_t frames, uint32_t tokens_per_frame, uint32_t block_size, int kind, int sink,
+                               uint32_t temporal_window, uint32_t spatial_window, void* stream, radial_layout** out) {
+    if (!out) return fail(RADIAL_ERR_INVALID, "null output handle");
+    *out = nullptr;
+    CacheEntry key{};
+    RADIAL_CUDA_TRY(cudaGetDevice(&key.dev));
+    key.f = frames;
+    key.s = tokens_per_frame;
+    key.B = block_size;
+    key.kind = kind;
+    key.sink = sink ? 1 : 0;
+    key.tw = temporal_window;
+    key.sw = spatial_window;
+    key.csr = false;
+    if ((*out = cache_find(key))) return RADIAL_OK;
+    radial_layout* L = nullptr;
+    int rc = radial_cuda_mask_build(frames, tokens_per_frame, block_size, kind, sink, temporal_window, spatial_window,
+                                    stream, &L);
+    if (rc) return rc;
+    *out = cache_insert(std::move(key), L);
+    return RADIAL_OK;
+}
+
+int radial_cuda_layout_acquire_csr(uint32_t frames, uint32_t tokens_per_frame, uint32_t block_size, int kind,
+                                   int sink, uint32_t grid_rows, const uint64_t* row_ptr, const uint32_t* col_idx,
+                                   void* stream, radial_layout** out) {
+    if (!out || !row_ptr) return fail(RADIAL_ERR_INVALID, "null argument");
+    *out = nullptr;
+    int rc = check_shape(frames, tokens_per_frame, block_size);
+    if (rc) return rc;
+    const uint64_t R = (static_cast<uint64_t>(frames) * tokens_per_frame + block_size - 1) / block_size;
+    if (grid_rows != R)
+        return radial_cuda_layout_from_csr(frames, tokens_per_frame, block_size, kind, sink, grid_rows, row_ptr,
+                                           col_idx, stream, out);  // reports the mismatch
+    CacheEntry key{};
+    RADIAL_CUDA_TRY(cudaGetDevice(&key.dev));
+    key.f = frames;
+    key.s = tokens_per_frame;
+    key.B = block_size;
+    key.kind = kind;
+    key.sink = sink ? 1 : 0;
+    key.csr = true;
+    key.rp.assign(row_ptr, row_ptr + R + 1);
+    if (row_ptr[R] && col_idx) key.ci.assign(col_idx, col_idx + row_ptr[R]);
+    if ((*out = cache_find(key))) return RADIAL_OK;
+    radial_layout* L = nullptr;
+    if ((rc = radial_cuda_layout_from_csr(frames, tokens_per_frame, block_size, kind, sink, grid_rows, row_ptr,
+                                          col_idx, stream, &L)))
+        return rc;
+    *out = cache_insert(std::move(key), L);
+    return RADIAL_OK;
+}
+
+void radial_cuda_layout_cache_clear(void) {
+    std::vector<radial_layout*> drop;
+    {
+        std::lock_guard<std::mutex> g(g_cache_mu);
+        for (auto& c : g_cache) drop.push_back(c.L);
+        g_cache.clear();
+    }
+    for (auto* d : drop) free_layout(d);
+}
+
+uint64_t radial_cuda_kernel_launches(void) { return g_launches.load(std::memory_order_relaxed); }
 
 int radial_cuda_layout_info(const radial_layout* L, radial_layout_info* info) {
     if (!L || !info) return fail(RADIAL_ERR_INVALID, "null argument");
@@ -391,8 +620,6 @@ int radial_cuda_attn_fwd_token(const void* q, const void* k, const void* v, void
     int rc = check_attn(q, k, v, o, heads, n, head_dim);
     if (rc) return rc;
     if ((rc = check_layout_for_attn(layout, n))) return rc;
-    if (layout->kind == RADIAL_KIND_POWER)
-        return fail(RADIAL_ERR_INVALID, "masked_attention: the power pattern has no per-frame span on the device path");
     if (!layout->from_pattern)
         return fail(RADIAL_ERR_INVALID, "masked_attention: token-exact mode needs a layout built by radial_cuda_mask_build");
     return launch_fwd(q, k, v, o, lse, heads, n, head_dim, layout->B, resolve_scale(scale, head_dim), layout,
@@ -445,8 +672,8 @@ int radial_cuda_attn_fwd_host_multi(const void* q, const void* k, const void* v,
         radial_layout* L = nullptr;
         if (cudaSetDevice(devices[r]) != cudaSuccess) {
             rcs[r] = fail(RADIAL_ERR_CUDA, "attn_fwd_host_multi: cudaSetDevice failed");
-        } else if ((e = radial_cuda_mask_build(frames, tokens_per_frame, block_size, kind, sink, temporal_window,
-                                               spatial_window, nullptr, &L)) != RADIAL_OK) {
+        } else if ((e = radial_cuda_layout_acquire(frames, tokens_per_frame, block_size, kind, sink, temporal_window,
+                                                   spatial_window, nullptr, &L)) != RADIAL_OK) {
             rcs[r] = e;
         } else {
             const size_t hb = static_cast<size_t>(n) * head_dim * 2 * h0;
@@ -477,8 +704,6 @@ int radial_cuda_attn_fwd_token_host(const void* q, const void* k, const void* v,
     int rc = check_attn(q, k, v, o, heads, n, head_dim);
     if (rc) return rc;
     if ((rc = check_layout_for_attn(layout, n))) return rc;
-    if (layout->kind == RADIAL_KIND_POWER)
-        return fail(RADIAL_ERR_INVALID, "masked_attention: the power pattern has no per-frame span on the device path");
     if (!layout->from_pattern)
         return fail(RADIAL_ERR_INVALID, "masked_attention: token-exact mode needs a layout built by radial_cuda_mask_build");
     return host_fwd(q, k, v, o, lse, heads, n, head_dim, layout->B, scale, layout,

@@ -3,8 +3,12 @@
 
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdint>
+#include <mutex>
 #include <string>
+#include <utility>
+#include <vector>
 
 #include "../../include/radial_cuda.h"
 
@@ -12,6 +16,14 @@
 // per (shape, pattern, block size) and is immutable afterwards.
 struct radial_layout {
     int device = 0;
+    // shared ownership: radial_cuda_layout_free drops one reference; the device layout cache
+    // (radial_cuda_layout_acquire*) holds one of its own
+    std::atomic<int> refs{1};
+    // streams this layout was last used on (one event each, re-recorded per launch): freeing
+    // waits for exactly those uses, stream-ordered, instead of synchronising the device
+    std::mutex use_mu;
+    std::vector<std::pair<cudaStream_t, cudaEvent_t>> uses;
+    uint64_t kept_offset = 0;  // row_ptr[0] of an uploaded CSR (deserialize accepts a nonzero start)
     uint32_t f = 1, s = 1, B = 1, R = 0;
     uint8_t kind = 0, sink = 1;
     uint32_t tw = 0, sw = 0;
@@ -34,10 +46,6 @@ struct radial_layout {
     uint32_t* uidx = nullptr;
     uint32_t* uorder = nullptr;   // chunks by descending list length within windows (LPT)
     uint32_t* uidx_asc = nullptr; // the same entries in ascending J (token-exact mode); uidx pairs solo entries
-    // Backward dK/dV work list: same over KV chunks using the CSC.
-    uint64_t* tptr = nullptr;
-    uint32_t* tidx = nullptr;
-    uint32_t* torder = nullptr;
     // Backward per-block orders (longest list first): CSR rows (dQ), CSC columns (dK/dV)
     uint32_t* rorder = nullptr;
     uint32_t* corder = nullptr;
@@ -55,6 +63,12 @@ struct FwdScatter {
 void set_error(const std::string& msg);
 int fail(int code, const std::string& msg);
 int cuda_fail(cudaError_t e, const char* where);
+
+// Records that `L` is read by work queued on `st` (skipped while `st` is capturing a graph:
+// layouts used by a captured graph must outlive it).
+void note_use(const radial_layout* L, cudaStream_t st);
+// Kernel launches issued by this library (radial_cuda_kernel_launches).
+void count_launches(uint64_t k);
 
 // mask_build.cu
 int build_layout_device(radial_layout* L, cudaStream_t st);

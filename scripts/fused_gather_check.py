@@ -16,6 +16,11 @@ def main():
     import paper_2506_19852_b200 as P
     from paper_2506_19852_b200.heads import HeadParallel
     hp = HeadParallel.from_env("nccl")
+    if "--expect-ranks" in sys.argv:
+        want = int(sys.argv[sys.argv.index("--expect-ranks") + 1])
+        if hp.world != want:
+            print(f"fused_gather_check: expected {want} ranks, launched with {hp.world}", file=sys.stderr)
+            sys.exit(2)
     if hp.world == 1 and not dist.is_initialized():
         torch.cuda.set_device(0)
         dist.init_process_group("nccl", device_id=torch.device("cuda", 0))

@@ -12,7 +12,7 @@ sys.path.insert(0, ROOT)
 def main():
     import torch
     import paper_2506_19852_b200 as P
-    lib = ctypes.CDLL(P.library_path())
+    lib = ctypes.CDLL(P.debug_library_path())
     out = torch.zeros(148 * 4, dtype=torch.int64, device="cuda")
     for mmas, mw in ((0, 1), (3000, 1), (3000, 3)):
         assert lib.radial_cuda_debug_mma_dispatch(mmas, 20000, mw, ctypes.c_void_p(out.data_ptr())) == 0

@@ -11,7 +11,7 @@ sys.path.insert(0, ROOT)
 def main():
     import torch
     import paper_2506_19852_b200 as P
-    lib = ctypes.CDLL(P.library_path())
+    lib = ctypes.CDLL(P.debug_library_path())
     out = torch.zeros(148, dtype=torch.int64, device="cuda")
     iters = 2000
     for mode, commits in ((0, 0), (0, 4), (1, 0), (1, 2), (1, 4), (1, 8)):

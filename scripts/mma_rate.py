@@ -10,7 +10,7 @@ sys.path.insert(0, ROOT)
 def main():
     import torch
     import paper_2506_19852_b200 as P
-    lib = ctypes.CDLL(P.library_path())
+    lib = ctypes.CDLL(P.debug_library_path())
     names = {0: "SS N=128", 1: "TS N=128", 2: "SS N=256", 3: "TS N=256"}
     for ctas in (148,):
         for mode in [0, 1, 2, 3, 4, 5, 6, 7, 8, 9]:

@@ -13,7 +13,7 @@ NAMES = ["ex2.f32", "ex2.f16x2", "ex2.bf16x2", "cvt.f16x2.f32", "cvt.bf16x2.f32"
 def main():
     import torch
     import paper_2506_19852_b200 as P
-    lib = ctypes.CDLL(P.library_path())
+    lib = ctypes.CDLL(P.debug_library_path())
     out = torch.zeros(148, dtype=torch.int64, device="cuda")
     iters = 4096
     for warps in (4, 8, 16):

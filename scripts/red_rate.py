@@ -10,7 +10,7 @@ sys.path.insert(0, ROOT)
 def main():
     import torch
     import paper_2506_19852_b200 as P
-    lib = ctypes.CDLL(P.library_path())
+    lib = ctypes.CDLL(P.debug_library_path())
     out = torch.zeros(148, dtype=torch.int64, device="cuda")
     for blocks in (929, 24 * 929):  # one head of H33 (61 MB) / all 24 heads (1.46 GB)
         buf = torch.zeros(blocks * 128 * 128, dtype=torch.float32, device="cuda")

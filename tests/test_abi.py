@@ -23,7 +23,7 @@ def test_library_exports_every_declared_symbol():
     assert len(syms) >= 15
     missing = [s for s in syms if not hasattr(lib, s)]
     assert not missing, missing
-    assert lib.radial_cuda_abi_version() == 1
+    assert lib.radial_cuda_abi_version() == 2
 
 
 def test_library_is_sm100a():

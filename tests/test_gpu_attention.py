@@ -35,7 +35,7 @@ def test_debug_tile_mma_building_blocks(P):
     """S = Q K^T (SS, K-major) and O = P V (TS, MN-major V) on one 128x128x128 tile."""
     import ctypes
     import torch
-    lib = ctypes.CDLL(P.library_path())
+    lib = ctypes.CDLL(P.debug_library_path())
     g = torch.Generator(device="cuda").manual_seed(0)
     q, k, v, p = (torch.randn(128, 128, device="cuda", generator=g).to(torch.bfloat16) for _ in range(4))
     s_out = torch.empty(128, 128, device="cuda")
@@ -262,13 +262,18 @@ def test_fused_reassembly_through_symmetric_memory():
     import subprocess
     import sys
     import torch
-    nproc = max(1, min(torch.cuda.device_count(), 8))
+    # RADIAL_TEST_RANKS pins the rank count (e.g. 8 on an 8-GPU node): fewer visible GPUs
+    # is a failure, not a silent single-rank run
+    want = os.environ.get("RADIAL_TEST_RANKS")
+    nproc = int(want) if want else max(1, min(torch.cuda.device_count(), 8))
+    assert torch.cuda.device_count() >= nproc, f"{nproc} ranks requested, {torch.cuda.device_count()} GPUs visible"
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
            "--master-addr", "127.0.0.1", "--master-port", "29561",
-           os.path.join(ROOT, "scripts", "fused_gather_check.py")]
+           os.path.join(ROOT, "scripts", "fused_gather_check.py"), "--expect-ranks", str(nproc)]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=240)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-4000:]
     assert '"identical": true' in r.stdout
+    assert f'"ranks": {nproc}' in r.stdout
 
 
 @pytest.mark.parametrize("f,s,H", [(21, 3600, 40), (28, 1590, 24), (132, 3600, 24)],

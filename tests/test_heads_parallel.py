@@ -64,3 +64,34 @@ def test_two_rank_gloo_head_parallel(heads):
     want = [[[float(h)] * 3] * 5 for h in range(heads)]
     assert full0 == want and full1 == want
     assert m0 == m1 == 3.0
+
+
+def _bench(args, env_extra=None):
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    env.update(env_extra or {})
+    return subprocess.run([sys.executable, os.path.join(root, "bench.py")] + args, capture_output=True, text=True,
+                          env=env, timeout=300)
+
+
+@pytest.mark.parametrize("n", [2, 3])
+def test_bench_spawns_its_own_ranks(n):
+    """`bench.py --gpus N` without torchrun re-launches itself with N ranks (the driver's
+    command shape) and every rank owns its share of the 24 heads (gloo, no GPU)."""
+    import json
+    r = _bench(["--gpus", str(n), "--dry-run"])
+    assert r.returncode == 0, r.stderr[-2000:]
+    line = json.loads(r.stdout.strip().splitlines()[-1])
+    assert line["n_gpus"] == n
+    spans = line["heads_per_rank"]
+    assert spans[0][0] == 0 and spans[-1][1] == 24
+    assert all(a[1] == b[0] for a, b in zip(spans, spans[1:]))
+    assert line["max_over_ranks"] == float(n)
+
+
+def test_bench_rejects_world_size_mismatch():
+    r = _bench(["--gpus", "2", "--dry-run"], {"WORLD_SIZE": "1", "RANK": "0", "LOCAL_RANK": "0"})
+    assert r.returncode == 2
+    assert "WORLD_SIZE=1" in r.stderr
