@@ -538,7 +538,7 @@ int ro_version(void) { return 1; }
 /* ------------------------------------------------------------------------ */
 /* attention.hpp:184-225  masked_attention(inst, PatternSpec): token-exact   */
 /* softmax over the keys of for_each_kept_interval (mask.hpp:238-272), for   */
-/* frame-structured kinds, restated for chosen query rows. fp32 inputs.      */
+/* every kind (power: mask.hpp:246-270), restated for chosen query rows.    */
 /* ------------------------------------------------------------------------ */
 typedef struct {
     uint64_t n;
@@ -552,42 +552,72 @@ typedef struct {
     int status;
 } ro_tok_ctx;
 
-static void ro_tok_row(void* vctx, uint64_t r) {
-    ro_tok_ctx* c = (ro_tok_ctx*)vctx;
-    const uint64_t u = c->rows[r];
-    const uint32_t d = c->d, s = c->s;
+/* Kept keys of query token u = (i, k) in the order for_each_kept_interval visits them        */
+/* (mask.hpp:238-272): frame-structured kinds walk kept_span per key frame; power             */
+/* (mask.hpp:246-270) keeps u and u +- 2^t, plus all of frame 0 under the sink.               */
+typedef void (*ro_key_fn)(void* st, uint64_t v);
+
+static void ro_tok_keys(const ro_tok_ctx* c, uint64_t u, ro_key_fn fn, void* st) {
+    const uint32_t s = c->s;
+    if (c->pat.kind == RO_KIND_POWER) {
+        if (c->pat.sink)
+            for (uint64_t v = 0; v < s; ++v) fn(st, v);
+        if (!(c->pat.sink && u < s)) fn(st, u);
+        for (uint64_t t = 1; t < c->n; t <<= 1) {
+            if (u >= t && !(c->pat.sink && u - t < s)) fn(st, u - t);
+            if (u + t < c->n && !(c->pat.sink && u + t < s)) fn(st, u + t);
+        }
+        return;
+    }
     const uint32_t i = (uint32_t)(u / s), kpos = (uint32_t)(u % s);
-    double* o = c->out + r * d;
-    for (uint32_t e = 0; e < d; ++e) o[e] = 0.0;
-    double m = -INFINITY;
-    /* pass 1: max over kept logits */
     for (uint32_t j = 0; j < c->f; ++j) {
         uint32_t lo, hi;
         if (ro_kept_span(c->pat.kind, c->pat.sink, c->pat.tw, c->pat.sw, s, i, kpos, kpos, j, &lo, &hi) != 1) continue;
-        for (uint64_t v = (uint64_t)j * s + lo; v <= (uint64_t)j * s + hi; ++v) {
-            double dot = 0.0;
-            for (uint32_t x = 0; x < d; ++x) dot += (double)c->q[u * d + x] * (double)c->k[v * d + x];
-            if (dot * c->scale > m) m = dot * c->scale;
-        }
+        for (uint64_t v = (uint64_t)j * s + lo; v <= (uint64_t)j * s + hi; ++v) fn(st, v);
     }
-    if (m == -INFINITY) {
+}
+
+typedef struct {
+    const ro_tok_ctx* c;
+    uint64_t u;
+    double m, denom;
+    double* o;
+} ro_tok_state;
+
+static double ro_tok_logit(const ro_tok_state* t, uint64_t v) {
+    const uint32_t d = t->c->d;
+    double dot = 0.0;
+    for (uint32_t x = 0; x < d; ++x) dot += (double)t->c->q[t->u * d + x] * (double)t->c->k[v * d + x];
+    return dot * t->c->scale;
+}
+
+static void ro_tok_max(void* vs, uint64_t v) {
+    ro_tok_state* t = (ro_tok_state*)vs;
+    const double lg = ro_tok_logit(t, v);
+    if (lg > t->m) t->m = lg;
+}
+
+static void ro_tok_acc(void* vs, uint64_t v) {
+    ro_tok_state* t = (ro_tok_state*)vs;
+    const uint32_t d = t->c->d;
+    const double w = exp(ro_tok_logit(t, v) - t->m);
+    t->denom += w;
+    for (uint32_t x = 0; x < d; ++x) t->o[x] += w * (double)t->c->v[v * d + x];
+}
+
+static void ro_tok_row(void* vctx, uint64_t r) {
+    ro_tok_ctx* c = (ro_tok_ctx*)vctx;
+    const uint32_t d = c->d;
+    ro_tok_state t = {c, c->rows[r], -INFINITY, 0.0, c->out + r * d};
+    for (uint32_t e = 0; e < d; ++e) t.o[e] = 0.0;
+    ro_tok_keys(c, t.u, ro_tok_max, &t); /* pass 1: max over kept logits */
+    if (t.m == -INFINITY) {
         c->status = 2;
         return;
     }
-    double denom = 0.0;
-    for (uint32_t j = 0; j < c->f; ++j) {
-        uint32_t lo, hi;
-        if (ro_kept_span(c->pat.kind, c->pat.sink, c->pat.tw, c->pat.sw, s, i, kpos, kpos, j, &lo, &hi) != 1) continue;
-        for (uint64_t v = (uint64_t)j * s + lo; v <= (uint64_t)j * s + hi; ++v) {
-            double dot = 0.0;
-            for (uint32_t x = 0; x < d; ++x) dot += (double)c->q[u * d + x] * (double)c->k[v * d + x];
-            double w = exp(dot * c->scale - m);
-            denom += w;
-            for (uint32_t x = 0; x < d; ++x) o[x] += w * (double)c->v[v * d + x];
-        }
-    }
-    for (uint32_t x = 0; x < d; ++x) o[x] /= denom;
-    if (c->lse) c->lse[r] = m + log(denom);
+    ro_tok_keys(c, t.u, ro_tok_acc, &t);
+    for (uint32_t x = 0; x < d; ++x) t.o[x] /= t.denom;
+    if (c->lse) c->lse[r] = t.m + log(t.denom);
 }
 
 int ro_token_attention_rows_f32(uint64_t n, uint32_t d, const float* q, const float* k, const float* v,
@@ -596,7 +626,6 @@ int ro_token_attention_rows_f32(uint64_t n, uint32_t d, const float* q, const fl
                                 double* lse) {
     ro_tok_ctx c = {n, d, f, s, q, k, v, {kind, sink, 1, 1, tw, sw}, rows, out, lse,
                     scale > 0 ? scale : 1.0 / sqrt((double)d), 0};
-    if (kind == RO_KIND_POWER) return -1;
     ro_parallel_for(n_rows, ro_tok_row, &c);
     return c.status;
 }

@@ -303,7 +303,7 @@ class DeviceLayout:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h is not None and h.value:
+        if h is not None and h.value and _lib is not None:  # _lib is None at interpreter teardown
             _lib.radial_cuda_layout_free(h)
             self._h = C.c_void_p(0)
 

@@ -459,7 +459,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         for (int i = 0; i < kDS; ++i) {
             mbar_init(&bar_dofull[i], 1);
-            mbar_init(&bar_doempty[i], 1);
+            // the MMA warp's commit (dV(i), dK(i) done with dO_i) plus the 8 elementwise warps
+            // (done reading the stage's lse2 / D): the generic reads are then ordered before
+            // the next bulk load into the stage directly, not only through the MMA chain
+            mbar_init(&bar_doempty[i], 1 + 8);
         }
         mbar_init(bar_s, 1);
         mbar_init(bar_sfree, 8);
@@ -658,7 +661,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             tmem_wait_st();
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(bar_ds);
+            if (lane == 0) {
+                mbar_arrive(bar_ds);
+                mbar_arrive(&bar_doempty[ds]);  // this warp's lse2 / D reads of the stage are done
+            }
             if ((warp == 4 || warp == 8) && lane == 0) BTRACE(warp == 4 ? 9 : 11, i);
         }
         // ---------------------------------------------------- epilogue: wg0 -> dV, wg1 -> dK * scale

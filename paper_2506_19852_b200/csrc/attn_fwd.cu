@@ -110,6 +110,7 @@ struct FwdParams {
     const uint64_t* uptr;
     const uint32_t* uidx;
     const uint32_t* order;
+    const uint8_t* ufull;  // token-exact mode: per entry, bit t = tile t keeps the whole block
     uint64_t n;
     uint32_t heads, R, C;
     float scale_log2;
@@ -502,10 +503,17 @@ __global__ void __launch_bounds__(kThreads, 1)
             if constexpr (TOKEN) {
                 // token-exact mode (masked_attention(inst, PatternSpec), attention.hpp:184-225):
                 // keep exactly the key intervals kept_span(i, k, k, j) of this row's token
-                // (i, k) in each key frame j the block overlaps (mask.hpp:238-272)
+                // (i, k) in each key frame j the block overlaps (mask.hpp:238-272).  K1 flags the
+                // entries whose whole tile keeps the whole block (ufull): those take the
+                // block path's unmasked code with no per-row mask.
+                const bool tile_full = (__ldg(p.ufull + ebase + j) >> t) & 1u;
 #pragma unroll
-                for (int w = 0; w < BK / 32; ++w) kmask[w] = 0u;
-                if (active && grow < p.n && p.rule.kind == RADIAL_KIND_POWER) {
+                for (int w = 0; w < BK / 32; ++w) {
+                    const int len = min(max(valid - 32 * w, 0), 32);
+                    kmask[w] = tile_full ? (len == 32 ? 0xffffffffu : ((1u << len) - 1u)) : 0u;
+                }
+                if (tile_full) {
+                } else if (active && grow < p.n && p.rule.kind == RADIAL_KIND_POWER) {
                     // power rule (mask.hpp:246-270): key v is kept iff |u - v| is 0 or a power of
                     // two, or (sink) v lies in frame 0
                     const uint64_t v0 = static_cast<uint64_t>(J) * BK, vn = static_cast<uint64_t>(valid);
@@ -787,6 +795,8 @@ int launch_fwd_t(const void* q, const void* k, const void* v, void* o, float* ls
     }
     if (token) {
         p.rule = radial_rule::MaskParams{L->f, L->s, L->B, n, L->kind, L->sink, L->tw, L->sw};
+        p.ufull = L->ufull;
+        if (!p.ufull) return fail(RADIAL_ERR_INVALID, "masked_attention: token-exact mode needs a layout built by radial_cuda_mask_build");
     }
     auto kern = token ? radial_attn_fwd_kernel<D, BK, true> : radial_attn_fwd_kernel<D, BK, false>;
     RADIAL_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmemAlloc));

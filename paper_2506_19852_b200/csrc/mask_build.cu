@@ -342,6 +342,57 @@ __global__ void __launch_bounds__(256) pair_solo_entries(const uint64_t* __restr
     }
 }
 
+// Token-exact fast path: for every entry of the ascending chunk lists, bit t is set iff Q tile
+// t (128 query rows of the chunk) keeps ALL token pairs of KV block J under the pattern's rule
+// (every block of the tile keeps J and span_covers holds for every frame pair the tile and
+// the block overlap).  The token-exact forward then skips its per-row mask for that tile.
+// One warp per chunk, lanes over the entries.
+__global__ void __launch_bounds__(256) token_full_flags(MaskParams p, const uint64_t* __restrict__ ptr, uint32_t C,
+                                                        uint32_t G, const uint32_t* __restrict__ idx,
+                                                        uint8_t* __restrict__ full) {
+    const uint32_t c = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint32_t lane = threadIdx.x & 31;
+    if (c >= C) return;
+    const uint32_t GT = G / 2;
+    const uint64_t s = p.s;
+    for (uint64_t e = ptr[c] + lane; e < ptr[c + 1]; e += 32) {
+        const uint32_t x = idx[e];
+        const uint32_t J = x & 0x0FFFFFFFu, m = x >> 28;
+        const uint64_t v0 = static_cast<uint64_t>(J) * p.B;
+        const uint64_t v1 = min(p.n, v0 + p.B) - 1;
+        uint8_t flags = 0;
+        for (uint32_t t = 0; t < 2; ++t) {
+            const uint64_t u0 = static_cast<uint64_t>(c) * 256 + t * 128;
+            if (u0 >= p.n) {
+                flags |= 1u << t;  // no query rows: vacuously full
+                continue;
+            }
+            if (((m >> (t * GT)) & ((1u << GT) - 1u)) != ((1u << GT) - 1u)) {
+                // some block of the tile skips J (or lies past the grid): only full if those
+                // blocks hold no rows
+                bool ok = true;
+                for (uint32_t g = 0; g < GT; ++g)
+                    if (!((m >> (t * GT + g)) & 1u) && u0 + static_cast<uint64_t>(g) * p.B < p.n) ok = false;
+                if (!ok) continue;
+            }
+            const uint64_t u1 = min(p.n, u0 + 128) - 1;
+            bool ok = true;
+            for (uint64_t i = u0 / s; ok && i * s <= u1; ++i) {
+                const uint32_t k_lo = static_cast<uint32_t>(max(u0, i * s) - i * s);
+                const uint32_t k_hi = static_cast<uint32_t>(min(u1, i * s + s - 1) - i * s);
+                for (uint64_t j = v0 / s; ok && j * s <= v1; ++j) {
+                    const uint32_t l_lo = static_cast<uint32_t>(max(v0, j * s) - j * s);
+                    const uint32_t l_hi = static_cast<uint32_t>(min(v1, j * s + s - 1) - j * s);
+                    ok = radial_rule::span_covers(p, static_cast<uint32_t>(i), k_lo, k_hi, static_cast<uint32_t>(j),
+                                                  l_lo, l_hi);
+                }
+            }
+            if (ok) flags |= 1u << t;
+        }
+        full[e] = flags;
+    }
+}
+
 // One list family (rows x cols under predicate F): counts -> exclusive scan into ptr.
 template <class F>
 int count_and_scan(F pred, uint32_t rows, uint32_t cols, uint32_t* counts, uint64_t* ptr, ScanStats* dstats,
@@ -455,7 +506,8 @@ int build_worklists(radial_layout* L, cudaStream_t st) {
     if ((rc = lpt_order(L->row_ptr, R, st, &L->rorder))) return rc;
     if ((rc = lpt_order(L->col_ptr, R, st, &L->corder))) return rc;
     if ((rc = lpt_order(L->uptr, C, st, &L->uorder))) return rc;
-    RADIAL_CUDA_TRY(cudaMemcpyAsync(sc.host, sc.stats, 3 * sizeof(ScanStats), cudaMemcpyDeviceToHost, st));
+    // slots 1 (CSC) and 2 (unions); slot 0 belongs to build_layout_device
+    RADIAL_CUDA_TRY(cudaMemcpyAsync(sc.host + 1, sc.stats + 1, 2 * sizeof(ScanStats), cudaMemcpyDeviceToHost, st));
     RADIAL_CUDA_TRY(cudaStreamSynchronize(st));
     if (sc.host[1].nnz != L->nnz) return fail(RADIAL_ERR_INVALID, "layout transpose size mismatch");
     const uint64_t un = sc.host[2].nnz;
@@ -473,6 +525,14 @@ int build_worklists(radial_layout* L, cudaStream_t st) {
         RADIAL_CUDA_TRY(cudaGetLastError());
         count_launches(1);
         RADIAL_CUDA_TRY(cudaFreeAsync(match, st));
+        if (L->from_pattern) {
+            const MaskParams mp{L->f, L->s, L->B, static_cast<uint64_t>(L->f) * L->s, L->kind, L->sink, L->tw, L->sw};
+            RADIAL_CUDA_TRY(cudaMallocAsync(&L->ufull, un, st));
+            token_full_flags<<<(C + warps_per_cta - 1) / warps_per_cta, 32 * warps_per_cta, 0, st>>>(
+                mp, L->uptr, C, L->G, L->uidx_asc, L->ufull);
+            RADIAL_CUDA_TRY(cudaGetLastError());
+            count_launches(1);
+        }
     }
     RADIAL_CUDA_TRY(cudaStreamSynchronize(st));
     return RADIAL_OK;

@@ -88,4 +88,18 @@ __host__ __device__ __forceinline__ bool kept_span(const MaskParams& p, uint32_t
     }
 }
 
+// Every query position k in [k_lo, k_hi] of frame i keeps every key position of
+// [l_lo, l_hi] in frame j (token level)?  kept_span's case depends on (i, j) only and, for a
+// fixed case, its interval ends are nondecreasing in k (band: [max(k - sigma, 0),
+// min(k + sigma, s - 1)]), so the extreme positions decide: the band of k_hi must start by
+// l_lo and the band of k_lo must reach l_hi.  Power has no per-frame span (never full here).
+__host__ __device__ __forceinline__ bool span_covers(const MaskParams& p, uint32_t i, uint32_t k_lo, uint32_t k_hi,
+                                                     uint32_t j, uint32_t l_lo, uint32_t l_hi) {
+    if (p.kind == RADIAL_KIND_POWER) return false;
+    uint32_t lo_a, hi_a, lo_b, hi_b;
+    if (!kept_span(p, i, k_hi, k_hi, j, lo_a, hi_a)) return false;
+    if (!kept_span(p, i, k_lo, k_lo, j, lo_b, hi_b)) return false;
+    return lo_a <= l_lo && hi_a >= l_hi && lo_b <= l_lo && hi_b >= l_hi;
+}
+
 }  // namespace radial_rule

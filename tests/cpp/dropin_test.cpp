@@ -3,6 +3,7 @@
 // libradial_cuda.so.  Restates the reference's own test logic
 // (tests/test_blocksparse.cpp, tests/test_attention.cpp) with independent oracles
 // written here.  Prints "PASS <name>" / "FAIL <name>: why"; exit code = #failures.
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <limits>
@@ -139,6 +140,33 @@ int main() {
         auto want = naive(inst, &tok, true);
         const double rel = rel_l2(got, want);
         report(rel < 1e-2, "masked_attention(inst, PatternSpec) token-exact rel-L2 " + std::to_string(rel));
+    }
+    // power kind, token-exact (mask.hpp:246-270): the B = 1 power layout is its token mask
+    for (bool sink : {false, true}) {
+        GridShape shape(5, 60);
+        auto inst = random_instance(shape, 64, 17);
+        auto got = masked_attention(inst, PatternSpec::power(sink));
+        auto tok = blockify(shape, PatternSpec::power(sink), 1);
+        const double rel = rel_l2(got, naive(inst, &tok, true));
+        report(rel < 1e-2, std::string("masked_attention(inst, power") + (sink ? "+sink" : "") +
+                               ") token-exact rel-L2 " + std::to_string(rel));
+    }
+    // the reference's per-head call pattern (one masked_attention per head, same layout): the
+    // device layout cache uploads the layout once, later heads skip the upload and work lists
+    {
+        GridShape shape(9, 360);
+        auto lay = blockify(shape, PatternSpec::radial(true), 128);
+        double first_ms = 0, rest_ms = 0, worst = 0;
+        for (int h = 0; h < 6; ++h) {
+            auto inst = random_instance(shape, 128, 100 + h);
+            auto t0 = std::chrono::steady_clock::now();
+            auto got = masked_attention(inst, lay);
+            const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+            (h == 0 ? first_ms : rest_ms) += ms;
+            if (h < 2) worst = std::max(worst, rel_l2(got, naive(inst, &lay, true)));
+        }
+        std::printf("per-head loop: first call %.2f ms, later calls %.2f ms each\n", first_ms, rest_ms / 5);
+        report(worst < 1e-2, "per-head masked_attention loop (cached layout) rel-L2 " + std::to_string(worst));
     }
     // dense_attention vs naive dense (test_attention.cpp:80-83 style)
     {

@@ -117,3 +117,20 @@ def test_scatter_forward_argument_validation():
     nulls = (VP * 2)(0x2000, 0)
     assert call(2, 0, 2, ptrs=nulls) == 1 and b"null destination" in lib.radial_cuda_last_error()
     assert call(1, 0, 2) == 1 and b"null layout" in lib.radial_cuda_last_error()
+
+
+@pytest.mark.parametrize("kind,tw,sw,msg", [(2, None, 0, "spatial pattern requires temporal_window"),
+                                            (3, 0, None, "temporal pattern requires spatial_window"),
+                                            (4, 1, None, "sta pattern requires spatial_window"),
+                                            (4, None, 3, "sta pattern requires temporal_window")])
+def test_mask_build_rejects_missing_windows(kind, tw, sw, msg):
+    """PatternSpec::validate (grid.hpp:118-139) through the C-ABI: RADIAL_WINDOW_NONE marks an
+    absent window; a kind that reads it fails with the reference's message (no CUDA call)."""
+    import paper_2506_19852_b200 as P
+    h = ctypes.c_void_p()
+    none = P.WINDOW_NONE
+    rc = P._lib.radial_cuda_mask_build(4, 16, 4, kind, 0, none if tw is None else tw, none if sw is None else sw,
+                                       None, ctypes.byref(h))
+    assert rc == P.ERR_INVALID
+    assert P._lib.radial_cuda_last_error().decode() == msg
+    assert not h.value

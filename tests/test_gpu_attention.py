@@ -330,14 +330,16 @@ def test_paper_scale_dense_comparator_sampled_rows(P):
 @pytest.mark.parametrize("f,s,B,d,kind,sink,tw,sw", [
     (8, 256, 64, 64, "radial", True, 0, 0), (6, 300, 128, 128, "radial", False, 0, 0),
     (33, 150, 128, 128, "radial", True, 0, 0), (5, 333, 64, 128, "sta", True, 1, 40),
-    (7, 200, 128, 64, "harmonic", False, 0, 0), (9, 100, 128, 128, "temporal", True, 0, 17)])
+    (7, 200, 128, 64, "harmonic", False, 0, 0), (9, 100, 128, 128, "temporal", True, 0, 17),
+    (7, 90, 128, 64, "power", True, 0, 0), (12, 50, 64, 128, "power", False, 0, 0)])
 def test_token_exact_forward_vs_oracle(P, f, s, B, d, kind, sink, tw, sw):
     """masked_attention(inst, PatternSpec) (attention.hpp:184-225) on the GPU: exact token mask."""
     import torch
     H = 2
     q, k, v = instance_bf16(f, s, d, H, 21)
     mk = {"radial": lambda: P.PatternSpec.radial(sink), "sta": lambda: P.PatternSpec.sta(tw, sw, sink),
-          "harmonic": lambda: P.PatternSpec.harmonic(sink), "temporal": lambda: P.PatternSpec.temporal(sw, sink)}
+          "harmonic": lambda: P.PatternSpec.harmonic(sink), "temporal": lambda: P.PatternSpec.temporal(sw, sink),
+          "power": lambda: P.PatternSpec.power(sink)}
     o, lse = P.masked_attention_pattern(to_torch_bf16(q), to_torch_bf16(k), to_torch_bf16(v), P.GridShape(f, s),
                                         mk[kind](), block_size=B, return_lse=True)
     torch.cuda.synchronize()
@@ -350,12 +352,12 @@ def test_token_exact_forward_vs_oracle(P, f, s, B, d, kind, sink, tw, sw):
 
 
 def test_token_exact_random_fuzz_vs_oracle(P):
-    """24 random token-exact cases over every frame-structured kind (radial, dense, spatial,
-    temporal, sta, harmonic) with random windows, sink, block and head_dim."""
+    """28 random token-exact cases over every kind (radial, dense, spatial, temporal, sta,
+    harmonic, power) with random windows, sink, block and head_dim."""
     import torch
     rng = np.random.default_rng(4242)
-    kinds = ["radial", "dense", "spatial", "temporal", "sta", "harmonic"]
-    for case in range(24):
+    kinds = ["radial", "dense", "spatial", "temporal", "sta", "harmonic", "power"]
+    for case in range(28):
         kind = kinds[case % len(kinds)]
         f = int(rng.integers(1, 14))
         s = int(rng.integers(2, 401))
@@ -368,7 +370,8 @@ def test_token_exact_random_fuzz_vs_oracle(P):
                 "spatial": lambda: P.PatternSpec.spatial(tw, sink),
                 "temporal": lambda: P.PatternSpec.temporal(sw, sink),
                 "sta": lambda: P.PatternSpec.sta(tw, sw, sink),
-                "harmonic": lambda: P.PatternSpec.harmonic(sink)}[kind]()
+                "harmonic": lambda: P.PatternSpec.harmonic(sink),
+                "power": lambda: P.PatternSpec.power(sink)}[kind]()
         q, k, v = instance_bf16(f, s, d, 1, 500 + case)
         try:
             o = P.masked_attention_pattern(to_torch_bf16(q), to_torch_bf16(k), to_torch_bf16(v), P.GridShape(f, s),
@@ -386,13 +389,15 @@ def test_token_exact_random_fuzz_vs_oracle(P):
 
 
 @pytest.mark.skipif(not O.ref_available(), reason="oracle/_ref not built")
-def test_token_exact_forward_vs_reference_library(P):
+@pytest.mark.parametrize("kind,sink", [("radial", True), ("power", True), ("power", False)])
+def test_token_exact_forward_vs_reference_library(P, kind, sink):
     import torch
     f, s, d = 8, 256, 64
     q, k, v = instance_bf16(f, s, d, 1, 42)
+    spec = P.PatternSpec.radial(sink) if kind == "radial" else P.PatternSpec.power(sink)
     o = P.masked_attention_pattern(to_torch_bf16(q), to_torch_bf16(k), to_torch_bf16(v), P.GridShape(f, s),
-                                   P.PatternSpec.radial(), block_size=64)
+                                   spec, block_size=64)
     torch.cuda.synchronize()
     ref = O.ref_masked_attention_pattern(f, s, q[0].astype(np.float64), k[0].astype(np.float64),
-                                         v[0].astype(np.float64))
+                                         v[0].astype(np.float64), kind, sink)
     assert_within(block_errors(o[0].float().cpu().numpy(), ref, np.arange(f * s), 64), "token vs reference")

@@ -170,3 +170,17 @@ def test_bwd_oracle_matches_torch_autograd_and_finite_differences():
     # forward output of the oracle equals torch's masked softmax
     fwd = O.attention_rows(q, k, v, B, rp, ci, np.arange(n))
     assert np.abs(fwd - o.detach().numpy()).max() < 1e-12
+
+
+@need_ref
+@pytest.mark.parametrize("kind,sink,tw,sw", [("power", False, 0, 0), ("power", True, 0, 0), ("radial", True, 0, 0),
+                                             ("sta", True, 1, 9), ("harmonic", False, 0, 0)])
+def test_token_attention_rows_match_reference_every_kind(kind, sink, tw, sw):
+    """The token-exact restatement (attention.hpp:184-225 over for_each_kept_interval,
+    mask.hpp:238-272, power included) equals the reference's own masked_attention(inst,
+    PatternSpec) on fp32-exact inputs."""
+    f, s, d = 6, 37, 16
+    q, k, v = (x.astype(np.float32).astype(np.float64) for x in O.random_instance(f * s, d, 9))
+    ref = O.ref_masked_attention_pattern(f, s, q, k, v, kind, sink, tw, sw)
+    mine = O.token_attention_rows(q, k, v, f, s, np.arange(f * s), kind, sink, tw, sw)
+    assert np.abs(mine - ref).max() < 1e-12
