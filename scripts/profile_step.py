@@ -15,6 +15,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="hunyuan33", choices=sorted(CONFIGS))
     ap.add_argument("--dense", action="store_true")
+    ap.add_argument("--token", action="store_true", help="token-exact forward (masked_attention_pattern)")
     ap.add_argument("--iters", type=int, default=1)
     a = ap.parse_args()
     import torch
@@ -25,6 +26,9 @@ def main():
     q, k, v = (torch.randn(H, n, d, device="cuda", generator=g).to(torch.bfloat16) for _ in range(3))
     lay = P.device_layout(P.GridShape(f, s), P.PatternSpec.radial(), B)
     for _ in range(a.iters):
+        if a.token:
+            P.masked_attention_pattern(q, k, v, P.GridShape(f, s), P.PatternSpec.radial(), block_size=B)
+            continue
         P.masked_attention(q, k, v, lay, return_lse=True)
         if a.dense:
             P.dense_attention(q, k, v, block_size=B, return_lse=True)
