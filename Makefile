@@ -6,7 +6,7 @@ NVCC ?= nvcc
 ARCH := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS := -O3 -std=c++17 $(ARCH) -lineinfo -Xcompiler -fPIC -Xptxas -v --expt-relaxed-constexpr
 CSRC := paper_2506_19852_b200/csrc
-SRCS := $(CSRC)/radial_cuda.cu $(CSRC)/mask_build.cu $(CSRC)/attn_fwd.cu $(CSRC)/attn_bwd.cu
+SRCS := $(CSRC)/radial_cuda.cu $(CSRC)/mask_build.cu $(CSRC)/attn_fwd.cu $(CSRC)/attn_fwd2.cu $(CSRC)/attn_bwd.cu
 HDRS := $(CSRC)/mask_rule.cuh $(CSRC)/sm100.cuh $(CSRC)/radial_internal.h include/radial_cuda.h
 LIB := paper_2506_19852_b200/lib/libradial_cuda.so
 DEBUG_LIB := paper_2506_19852_b200/lib/libradial_debug.so

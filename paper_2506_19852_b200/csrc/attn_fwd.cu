@@ -25,6 +25,7 @@
 // epilogue stores O rows straight into several ranks' full-O buffers (fused
 // head-parallel reassembly, radial_cuda_attn_fwd_scatter).
 #include <cmath>
+#include <cstdlib>
 #include <type_traits>
 
 #include "mask_rule.cuh"
@@ -817,6 +818,18 @@ extern "C" int radial_cuda_debug_trace(void* buf) {
 }
 #endif
 
+int launch_fwd_pair(const void* q, const void* k, const void* v, void* o, float* lse, uint32_t heads, uint64_t n,
+                    float scale, const radial_layout* L, cudaStream_t st, const FwdScatter* sc);
+
+// CTA-pair kernel (attn_fwd2.cu) for the paper shapes unless RADIAL_FWD_PAIR=0.
+bool use_pair_kernel() {
+    static const bool on = [] {
+        const char* e = getenv("RADIAL_FWD_PAIR");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
 int launch_fwd(const void* q, const void* k, const void* v, void* o, float* lse, uint32_t heads,
                uint64_t n, uint32_t D, uint32_t BK, float scale, const radial_layout* L,
                cudaStream_t st, bool token, const FwdScatter* sc) {
@@ -825,6 +838,8 @@ int launch_fwd(const void* q, const void* k, const void* v, void* o, float* lse,
     const uint32_t R = static_cast<uint32_t>(R64);
     if (sc && (sc->n_dst < 1 || sc->n_dst > static_cast<uint32_t>(kMaxDst)))
         return fail(RADIAL_ERR_INVALID, "attn_fwd_scatter: 1..8 destination buffers");
+    if (D == 128 && BK == 128 && !token && use_pair_kernel())
+        return launch_fwd_pair(q, k, v, o, lse, heads, n, scale, L, st, sc);
     if (D == 128 && BK == 128) return launch_fwd_t<128, 128>(q, k, v, o, lse, heads, n, scale, L, R, token, st, sc);
     if (D == 128 && BK == 64) return launch_fwd_t<128, 64>(q, k, v, o, lse, heads, n, scale, L, R, token, st, sc);
     if (D == 64 && BK == 128) return launch_fwd_t<64, 128>(q, k, v, o, lse, heads, n, scale, L, R, token, st, sc);

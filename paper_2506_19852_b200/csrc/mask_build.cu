@@ -446,8 +446,8 @@ int lpt_order(const uint64_t* dptr, uint32_t n, cudaStream_t st, uint32_t** orde
 struct Scratch {
     cudaStream_t st;
     uint32_t* counts = nullptr;
-    ScanStats* stats = nullptr;  // [3] CSR, CSC, query-chunk unions
-    ScanStats host[3];
+    ScanStats* stats = nullptr;  // [4] CSR, CSC, 256-row chunk unions, 512-row chunk unions
+    ScanStats host[4];
     explicit Scratch(cudaStream_t s) : st(s) {}
     ~Scratch() {
         if (counts) cudaFreeAsync(counts, st);
@@ -487,8 +487,11 @@ int build_worklists(radial_layout* L, cudaStream_t st) {
     L->G = attn ? 256 / L->B : 1;
     L->C = attn ? (R + L->G - 1) / L->G : 0;
     const uint32_t C = L->C;
-    RADIAL_CUDA_TRY(cudaMallocAsync(&sc.counts, sizeof(uint32_t) * (std::max<uint32_t>(R, 1) + std::max<uint32_t>(C, 1)), st));
-    RADIAL_CUDA_TRY(cudaMallocAsync(&sc.stats, 3 * sizeof(ScanStats), st));
+    L->C4 = L->B == 128 ? (R + 3) / 4 : 0;
+    const uint32_t C4 = L->C4;
+    RADIAL_CUDA_TRY(cudaMallocAsync(&sc.counts, sizeof(uint32_t) * (std::max<uint32_t>(R, 1) + std::max<uint32_t>(C, 1) +
+                                                                     std::max<uint32_t>(C4, 1)), st));
+    RADIAL_CUDA_TRY(cudaMallocAsync(&sc.stats, 4 * sizeof(ScanStats), st));
     RADIAL_CUDA_TRY(cudaMallocAsync(&L->col_ptr, sizeof(uint64_t) * (static_cast<size_t>(R) + 1), st));
     RADIAL_CUDA_TRY(cudaMallocAsync(&L->row_idx, sizeof(uint32_t) * std::max<uint64_t>(L->nnz, 1), st));
     int rc;
@@ -506,8 +509,14 @@ int build_worklists(radial_layout* L, cudaStream_t st) {
     if ((rc = lpt_order(L->row_ptr, R, st, &L->rorder))) return rc;
     if ((rc = lpt_order(L->col_ptr, R, st, &L->corder))) return rc;
     if ((rc = lpt_order(L->uptr, C, st, &L->uorder))) return rc;
-    // slots 1 (CSC) and 2 (unions); slot 0 belongs to build_layout_device
-    RADIAL_CUDA_TRY(cudaMemcpyAsync(sc.host + 1, sc.stats + 1, 2 * sizeof(ScanStats), cudaMemcpyDeviceToHost, st));
+    const ChunkUnion uq4{L->row_ptr, L->col_idx, R, 4};
+    if (C4) {
+        RADIAL_CUDA_TRY(cudaMallocAsync(&L->u4ptr, sizeof(uint64_t) * (static_cast<size_t>(C4) + 1), st));
+        if ((rc = count_and_scan(uq4, C4, R, sc.counts + R + C, L->u4ptr, sc.stats + 3, st))) return rc;
+        if ((rc = lpt_order(L->u4ptr, C4, st, &L->u4order))) return rc;
+    }
+    // slots 1 (CSC), 2 and 3 (unions); slot 0 belongs to build_layout_device
+    RADIAL_CUDA_TRY(cudaMemcpyAsync(sc.host + 1, sc.stats + 1, (C4 ? 3 : 2) * sizeof(ScanStats), cudaMemcpyDeviceToHost, st));
     RADIAL_CUDA_TRY(cudaStreamSynchronize(st));
     if (sc.host[1].nnz != L->nnz) return fail(RADIAL_ERR_INVALID, "layout transpose size mismatch");
     const uint64_t un = sc.host[2].nnz;
@@ -516,6 +525,10 @@ int build_worklists(radial_layout* L, cudaStream_t st) {
     // ascending lists (token-exact forward) filled directly, then the paired copy for the
     // block-layout forward
     if ((rc = fill(uq, C, R, L->uptr, L->uidx_asc, 1, st))) return rc;
+    if (C4) {
+        RADIAL_CUDA_TRY(cudaMallocAsync(&L->u4idx, sizeof(uint32_t) * std::max<uint64_t>(sc.host[3].nnz, 1), st));
+        if ((rc = fill(uq4, C4, R, L->u4ptr, L->u4idx, 1, st))) return rc;
+    }
     if (C && un) {
         uint32_t* match = nullptr;
         RADIAL_CUDA_TRY(cudaMallocAsync(&match, sizeof(uint32_t) * un, st));

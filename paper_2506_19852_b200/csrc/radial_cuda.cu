@@ -100,7 +100,8 @@ void free_layout(radial_layout* L) {
         L->uses.clear();
     }
     void* ptrs[] = {L->row_ptr, L->col_idx, L->col_ptr, L->row_idx, L->uptr,
-                    L->uidx,    L->uorder,  L->rorder,  L->corder,  L->uidx_asc, L->ufull};
+                    L->uidx,    L->uorder,  L->rorder,  L->corder,  L->uidx_asc, L->ufull,
+                    L->u4ptr,   L->u4idx,   L->u4order};
     for (void* p : ptrs)
         if (p) cudaFreeAsync(p, fs);
     cudaGetLastError();  // teardown at process exit may find the context gone

@@ -46,6 +46,11 @@ struct radial_layout {
     uint32_t* uidx = nullptr;
     uint32_t* uorder = nullptr;   // chunks by descending list length within windows (LPT)
     uint32_t* uidx_asc = nullptr; // the same entries in ascending J (token-exact mode); uidx pairs solo entries
+    // CTA-pair forward (block 128): 512-row chunk unions (4 query blocks, mask bits 28-31)
+    uint32_t C4 = 0;
+    uint64_t* u4ptr = nullptr;    // [C4+1]
+    uint32_t* u4idx = nullptr;
+    uint32_t* u4order = nullptr;
     uint8_t* ufull = nullptr;     // per uidx_asc entry, bit t: Q tile t keeps every token pair of the
                                   // 128 x B block at token level (token-exact fast path)
     // Backward per-block orders (longest list first): CSR rows (dQ), CSC columns (dK/dV)
