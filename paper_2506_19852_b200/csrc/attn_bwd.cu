@@ -661,6 +661,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             tmem_wait_st();
             tc_fence_before();
             __syncwarp();
+            fence_proxy_async_smem();  // the stage's lse2 / D reads before the next bulk load into it
+            __syncwarp();
             if (lane == 0) {
                 mbar_arrive(bar_ds);
                 mbar_arrive(&bar_doempty[ds]);  // this warp's lse2 / D reads of the stage are done

@@ -81,6 +81,11 @@ __device__ __forceinline__ void tma_load_3d_hint(void* smem_dst, const CUtensorM
         "l"(policy)
         : "memory");
 }
+// Orders this thread's generic-proxy shared-memory accesses before later async-proxy
+// (TMA / bulk copy) accesses to the same memory, and vice versa.
+__device__ __forceinline__ void fence_proxy_async_smem() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
 // 1-D bulk copy global -> shared (size multiple of 16, 16 B aligned), completing on bar.
 __device__ __forceinline__ void bulk_load(void* smem_dst, const void* src, uint32_t bytes, uint64_t* bar) {
     asm volatile(
