@@ -2,6 +2,7 @@
 #   make            -> paper_2506_19852_b200/lib/libradial_cuda.so + oracle
 #   make lib        -> CUDA library only
 #   make debug      -> diagnostics library (tcgen05 / pipe microbenchmarks, scripts/ only)
+#   make cli        -> paper_2506_19852_b200/lib/radial_cli (native mask / stats / bench CLI)
 NVCC ?= nvcc
 ARCH := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS := -O3 -std=c++17 $(ARCH) -lineinfo -Xcompiler -fPIC -Xptxas -v --expt-relaxed-constexpr
@@ -10,14 +11,20 @@ SRCS := $(CSRC)/radial_cuda.cu $(CSRC)/mask_build.cu $(CSRC)/attn_fwd.cu $(CSRC)
 HDRS := $(CSRC)/mask_rule.cuh $(CSRC)/sm100.cuh $(CSRC)/radial_internal.h include/radial_cuda.h
 LIB := paper_2506_19852_b200/lib/libradial_cuda.so
 DEBUG_LIB := paper_2506_19852_b200/lib/libradial_debug.so
+CLI := paper_2506_19852_b200/lib/radial_cli
 OBJDIR := build/obj
 OBJS := $(patsubst $(CSRC)/%.cu,$(OBJDIR)/%.o,$(SRCS))
 
-all: lib debug oracle
+all: lib debug cli oracle
 
 lib: $(LIB)
 
 debug: $(DEBUG_LIB)
+
+cli: $(CLI)
+
+$(CLI): tools/radial_cli.cpp $(LIB) include/radial/*.hpp include/radial_cuda.h
+	g++ -std=c++20 -O2 -Wall -Iinclude -o $@ tools/radial_cli.cpp -L$(dir $(LIB)) -lradial_cuda -Wl,-rpath,'$$ORIGIN'
 
 $(OBJDIR)/%.o: $(CSRC)/%.cu $(HDRS)
 	@mkdir -p $(OBJDIR)
@@ -36,10 +43,10 @@ oracle:
 	$(MAKE) -C oracle
 
 clean:
-	rm -rf build $(LIB) $(DEBUG_LIB)
+	rm -rf build $(LIB) $(DEBUG_LIB) $(CLI)
 	$(MAKE) -C oracle clean
 
-.PHONY: all lib debug oracle clean
+.PHONY: all lib debug cli oracle clean
 
 # kernel-variant libraries for tuning sweeps: make variant V=poly2 DEFS="-DRADIAL_POLY_PAIRS=2"
 variant:

@@ -821,11 +821,12 @@ extern "C" int radial_cuda_debug_trace(void* buf) {
 int launch_fwd_pair(const void* q, const void* k, const void* v, void* o, float* lse, uint32_t heads, uint64_t n,
                     float scale, const radial_layout* L, cudaStream_t st, const FwdScatter* sc);
 
-// CTA-pair kernel (attn_fwd2.cu) for the paper shapes unless RADIAL_FWD_PAIR=0.
+// CTA-pair kernel (attn_fwd2.cu): opt-in with RADIAL_FWD_PAIR=1 (measured slower than the
+// one-CTA kernel at every BASELINE shape).
 bool use_pair_kernel() {
     static const bool on = [] {
         const char* e = getenv("RADIAL_FWD_PAIR");
-        return !(e && e[0] == '0');
+        return e && e[0] == '1';
     }();
     return on;
 }

@@ -1,8 +1,8 @@
 """Forward timing at a BASELINE config for the kernel this process selects
-(RADIAL_FWD_PAIR=0: one-CTA K2; default: the CTA-pair kernel), sparse and dense, plus a
+(default: one-CTA K2; RADIAL_FWD_PAIR=1: the CTA-pair kernel), sparse and dense, plus a
 checksum of O so two runs can be compared.
 
-    python scripts/fwd_ab.py [--config hunyuan33] ; RADIAL_FWD_PAIR=0 python scripts/fwd_ab.py
+    python scripts/fwd_ab.py [--config hunyuan33] ; RADIAL_FWD_PAIR=1 python scripts/fwd_ab.py
 """
 import argparse
 import json
@@ -45,7 +45,7 @@ def main():
     torch.cuda.synchronize()
     fl = 4.0 * lay.kept_blocks() * B * B * d * H
     ts = timeit(lambda: P.masked_attention(q, k, v, lay, out=o, lse=lse, return_lse=True), a.iters)
-    rec = {"config": a.config, "pair": os.environ.get("RADIAL_FWD_PAIR", "1") != "0",
+    rec = {"config": a.config, "pair": os.environ.get("RADIAL_FWD_PAIR", "0") == "1",
            "sparse_ms": ts, "sparse_tflops": fl / ts / 1e9,
            "o_sum": float(o.float().sum()), "o_abs": float(o.float().abs().sum()), "lse_sum": float(lse.sum())}
     if not a.no_dense:

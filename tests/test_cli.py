@@ -1,5 +1,6 @@
-"""The GPU CLI (paper_2506_19852_b200/cli.py) keeps the reference CLI's flags, JSON keys and
-exit codes (tools/radial_cli.cpp, tests/test_cli.cpp)."""
+"""Both GPU CLIs -- the native one (tools/radial_cli.cpp -> paper_2506_19852_b200/lib/radial_cli,
+C++ over the drop-in headers) and the Python mirror (paper_2506_19852_b200/cli.py) -- keep the
+reference CLI's flags, JSON keys and exit codes (reference tools/radial_cli.cpp, tests/test_cli.cpp)."""
 import json
 import os
 import subprocess
@@ -11,15 +12,25 @@ import pytest
 import oracle as O
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+NATIVE = os.path.join(ROOT, "paper_2506_19852_b200", "lib", "radial_cli")
 
 
-def _cli(*args):
-    r = subprocess.run([sys.executable, "-m", "paper_2506_19852_b200.cli", *args], capture_output=True,
-                       text=True, cwd=ROOT, timeout=600)
-    return r.returncode, r.stdout, r.stderr
+@pytest.fixture(params=["native", "python"])
+def _cli(request):
+    if request.param == "native":
+        if not os.path.exists(NATIVE):
+            subprocess.run(["make", "-C", ROOT, "cli"], check=True, capture_output=True)
+        prefix = [NATIVE]
+    else:
+        prefix = [sys.executable, "-m", "paper_2506_19852_b200.cli"]
+
+    def run(*args):
+        r = subprocess.run([*prefix, *args], capture_output=True, text=True, cwd=ROOT, timeout=600)
+        return r.returncode, r.stdout, r.stderr
+    return run
 
 
-def test_stats_from_ramk_file_matches_reference_keys(tmp_path):
+def test_stats_from_ramk_file_matches_reference_keys(tmp_path, _cli):
     rp, ci = O.blockify(33, 3600, 128)
     path = tmp_path / "h33.ramk"
     path.write_bytes(O.serialize(33, 3600, 128, "radial", True, rp, ci))
@@ -30,7 +41,7 @@ def test_stats_from_ramk_file_matches_reference_keys(tmp_path):
     assert j["kept_blocks"] == 389411 and j["sparse_flops"] == pytest.approx(7.8399e13, rel=1e-4)
 
 
-def test_usage_and_input_errors_exit_2(tmp_path):
+def test_usage_and_input_errors_exit_2(tmp_path, _cli):
     assert _cli("stats", "--pattern", "nope", "--frames", "2", "--tokens", "2")[0] == 2
     assert _cli("stats")[0] == 2  # no shape
     assert _cli("frobnicate")[0] == 2
@@ -41,7 +52,7 @@ def test_usage_and_input_errors_exit_2(tmp_path):
 
 
 @pytest.mark.gpu
-def test_stats_presets_match_reference_acceptance_values():
+def test_stats_presets_match_reference_acceptance_values(_cli):
     # acceptance_main.cpp:182-212: hunyuan-509 reduction ~4.46x (formula), sparsities 59.6/68.0/77.6%
     rc, out, _ = _cli("stats", "--preset", "hunyuan-509", "--head-dim", "128")
     assert rc == 0
@@ -51,7 +62,7 @@ def test_stats_presets_match_reference_acceptance_values():
 
 
 @pytest.mark.gpu
-def test_mask_writes_reference_bytes_and_pgm(tmp_path):
+def test_mask_writes_reference_bytes_and_pgm(tmp_path, _cli):
     out, pgm = tmp_path / "m.ramk", tmp_path / "m.pgm"
     rc, so, err = _cli("mask", "--frames", "256", "--tokens", "64", "--block", "64", "--out", str(out), "--pgm", str(pgm))
     assert rc == 0, err
@@ -64,7 +75,7 @@ def test_mask_writes_reference_bytes_and_pgm(tmp_path):
 
 
 @pytest.mark.gpu
-def test_bench_emits_reference_keys():
+def test_bench_emits_reference_keys(_cli):
     rc, out, err = _cli("bench", "--frames", "16", "--tokens", "256", "--head-dim", "64", "--block", "64")
     assert rc == 0, err
     j = json.loads(out)
