@@ -632,3 +632,45 @@ extern "C" int radial_cuda_debug_red_rate(int mode, float* buf, uint32_t blocks,
     RADIAL_CUDA_TRY(cudaDeviceSynchronize());
     return RADIAL_OK;
 }
+
+// ---------------------------------------------------------------- racecheck probe
+// The smallest instance of K3's lse2 / D staging: lane 0 of warp 0 bulk-copies 512 B into
+// shared memory (completion on an mbarrier), warp 1 waits on that mbarrier and reads the
+// bytes; then a second round re-fills the same buffer after warp 1 has released it through a
+// second mbarrier (fence.proxy.async first), as the dK/dV ring does.  Correct by the
+// mbarrier / async-proxy rules; run under compute-sanitizer --tool racecheck to see whether
+// the tool reports it (scripts/racecheck_probe.py).
+namespace {
+__global__ void racecheck_probe_kernel(const float* src, float* out) {
+    __shared__ alignas(128) float buf[128];
+    __shared__ alignas(8) uint64_t full, empty;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        mbar_init(&full, 1);
+        mbar_init(&empty, 32);
+        fence_barrier_init();
+    }
+    __syncthreads();
+    for (int round = 0; round < 2; ++round) {
+        if (warp == 0 && lane == 0) {
+            if (round) mbar_wait(&empty, 0);
+            mbar_arrive_expect_tx(&full, 512);
+            bulk_load(buf, src + 128 * round, 512, &full);
+        } else if (warp == 1) {
+            mbar_wait(&full, round & 1);
+            float acc = 0.f;
+            for (int x = 0; x < 4; ++x) acc += buf[lane * 4 + x];
+            out[round * 32 + lane] = acc;
+            fence_proxy_async_smem();
+            mbar_arrive(&empty);
+        }
+    }
+}
+}  // namespace
+
+extern "C" int radial_cuda_debug_racecheck_probe(const float* src, float* out) {
+    racecheck_probe_kernel<<<1, 64>>>(src, out);
+    RADIAL_CUDA_TRY(cudaGetLastError());
+    RADIAL_CUDA_TRY(cudaDeviceSynchronize());
+    return RADIAL_OK;
+}

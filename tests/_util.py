@@ -57,3 +57,25 @@ def assert_within(errs: dict, what: str):
         f"{what}: worst per-block max-abs {worst_abs:.3e} (<= {MAX_ABS}), "
         f"rel-L2 {worst_rel:.3e} (<= {REL_L2})")
     return worst_abs, worst_rel
+
+
+def bf16_pipeline_bwd(q, k, v, do, B, row_ptr, col_idx):
+    """The backward's bf16 noise floor: exact fp64 math except at the points where K3 rounds
+    (O stored as bf16 by the forward and used for D = rowsum(dO*O); P and dS rounded to bf16 as
+    MMA operands; P from an fp32 exponent).  Dense n x n restatement, small shapes only."""
+    n, d = q.shape
+    sc = 1.0 / np.sqrt(d)
+    mask = np.zeros((n, n), bool)
+    for I in range(len(row_ptr) - 1):
+        for J in col_idx[row_ptr[I]:row_ptr[I + 1]]:
+            mask[I * B:(I + 1) * B, int(J) * B:(int(J) + 1) * B] = True
+    q64, k64, v64, do64 = (x.astype(np.float64) for x in (q, k, v, do))
+    S = np.where(mask, (q64 @ k64.T) * sc, -np.inf)
+    e = np.exp(S - S.max(1, keepdims=True))
+    p = e / e.sum(1, keepdims=True)
+    o_b = O.bf16_round((p @ v64).astype(np.float32)).astype(np.float64)
+    p32 = p.astype(np.float32).astype(np.float64)
+    ds = p32 * (do64 @ v64.T - (do64 * o_b).sum(1, keepdims=True))
+    p_b = O.bf16_round(p32.astype(np.float32)).astype(np.float64)
+    ds_b = O.bf16_round(ds.astype(np.float32)).astype(np.float64)
+    return (ds_b @ k64) * sc, (ds_b.T @ q64) * sc, p_b.T @ do64
