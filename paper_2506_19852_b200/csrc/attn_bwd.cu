@@ -443,7 +443,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint64_t* bar_p = bars + 14;       // [2] P^T(i) query halves in TMEM (8 each)
     uint64_t* bar_ds = bars + 16;      // dS^T(i) in TMEM (8)
     uint64_t* bar_acc = bars + 17;     // dV, dK final
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 18);
+    uint64_t* bar_vecempty = bars + 18;  // [2] the stage's lse2 / D read by the 8 elementwise warps
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 20);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t head = blockIdx.x / p.R;
@@ -459,10 +460,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         for (int i = 0; i < kDS; ++i) {
             mbar_init(&bar_dofull[i], 1);
-            // the MMA warp's commit (dV(i), dK(i) done with dO_i) plus the 8 elementwise warps
-            // (done reading the stage's lse2 / D): the generic reads are then ordered before
-            // the next bulk load into the stage directly, not only through the MMA chain
-            mbar_init(&bar_doempty[i], 1 + 8);
+            mbar_init(&bar_doempty[i], 1);   // the MMA warp's commit: dV(i), dK(i) done with dO_i
+            // the 8 elementwise warps, done reading the stage's lse2 / D (generic proxy); a
+            // barrier of their own, so the next bulk load into the stage is ordered after those
+            // reads by plain thread arrivals (not mixed with the tcgen05.commit arrival)
+            mbar_init(&bar_vecempty[i], 8);
         }
         mbar_init(bar_s, 1);
         mbar_init(bar_sfree, 8);
@@ -497,6 +499,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     tma_load_3d(smem + kOffQ + qs * T + a * Cfg::kAtomBytes, &tm_q, &bar_qfull[qs], a * 64,
                                 Iq * kBlk, head);
                 mbar_wait(&bar_doempty[ds], ((i / kDS) & 1) ^ 1);
+                mbar_wait(&bar_vecempty[ds], ((i / kDS) & 1) ^ 1);
                 mbar_arrive_expect_tx(&bar_dofull[ds], T + 2 * kBlk * 4);
                 for (int a = 0; a < Cfg::kAtoms; ++a)
                     tma_load_3d(smem + kOffDO + ds * T + a * Cfg::kAtomBytes, &tm_do, &bar_dofull[ds], a * 64,
@@ -665,7 +668,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             __syncwarp();
             if (lane == 0) {
                 mbar_arrive(bar_ds);
-                mbar_arrive(&bar_doempty[ds]);  // this warp's lse2 / D reads of the stage are done
+                mbar_arrive(&bar_vecempty[ds]);  // this warp's lse2 / D reads of the stage are done
             }
             if ((warp == 4 || warp == 8) && lane == 0) BTRACE(warp == 4 ? 9 : 11, i);
         }
@@ -752,7 +755,7 @@ int launch_bwd_t(const void* q, const void* k, const void* v, const void* o, con
     if (getenv("RADIAL_BWD_DQ_ONLY")) return RADIAL_OK;  // trace builds: time the dQ kernel alone
 #endif
     {
-        const int smem = 7 * T + 2048 + 160;  // K, V, 3 Q, 2 dO, lse2/D, barriers (no align slack)
+        const int smem = 7 * T + 2048 + 176;  // K, V, 3 Q, 2 dO, lse2/D, 20 barriers + TMEM slot (no align slack)
         auto kern = radial_attn_bwd_dkdv_kernel<D>;
         RADIAL_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         p.ptr = L->col_ptr;

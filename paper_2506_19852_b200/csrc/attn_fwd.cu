@@ -174,23 +174,28 @@ __global__ void __launch_bounds__(kThreads, 1)
     // windows of 2 x (SM count) consecutive chunks (LPT for a short grid tail, windowed so the
     // resident CTAs' K/V stays in L2 when a head does not: H132, 243 MB per head).
     const uint32_t item = blockIdx.x;
-    const uint32_t head = item / p.C;
-    const uint32_t chunk = p.order ? p.order[item % p.C] : item % p.C;
-    const uint64_t row0 = static_cast<uint64_t>(chunk) * 256;
-    uint64_t ebase = 0;
-    uint32_t L;
-    uint32_t dense_mask = 0;
-    if (p.dense) {
-        L = p.R;
-        for (int g = 0; g < Cfg::G; ++g)
-            if (chunk * Cfg::G + g < p.R) dense_mask |= 1u << g;
-    } else {
-        ebase = p.uptr[chunk];
-        L = static_cast<uint32_t>(p.uptr[chunk + 1] - ebase);
-    }
-    auto entry = [&](uint32_t j) -> uint32_t {
-        return p.dense ? (j | (dense_mask << 28)) : __ldg(p.uidx + ebase + j);
-    };
+    // The work item's list is (re)derived inside each warp role, after its setmaxnreg: values
+    // live across the role split were kept in local memory by ptxas (3 LDL per softmax step).
+#define FWD_WORK_ITEM                                                                  \
+    const uint32_t head = item / p.C;                                                  \
+    const uint32_t chunk = p.order ? __ldg(p.order + item % p.C) : item % p.C;         \
+    const uint64_t row0 = static_cast<uint64_t>(chunk) * 256;                          \
+    uint64_t ebase = 0;                                                                \
+    uint32_t L;                                                                        \
+    uint32_t dense_mask = 0;                                                           \
+    if (p.dense) {                                                                     \
+        L = p.R;                                                                       \
+        for (int g = 0; g < Cfg::G; ++g)                                               \
+            if (chunk * Cfg::G + g < p.R) dense_mask |= 1u << g;                       \
+    } else {                                                                           \
+        ebase = __ldg(p.uptr + chunk);                                                 \
+        L = static_cast<uint32_t>(__ldg(p.uptr + chunk + 1) - ebase);                  \
+    }                                                                                  \
+    auto entry = [&](uint32_t j) -> uint32_t {                                         \
+        return p.dense ? (j | (dense_mask << 28)) : __ldg(p.uidx + ebase + j);        \
+    };                                                                                 \
+    (void)head;                                                                        \
+    (void)row0
 
     if (warp == 0 && lane == 0) {
         mbar_init(bar_q, 1);
@@ -221,6 +226,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // each (128 x 72 + 256 x 216 <= 64K; measured +1% over 104 / 200, no spills)
     if (warp < 4) {
         regs_dec<RADIAL_FWD_REGS_LO>();
+        FWD_WORK_ITEM;
     if (warp == 0) {
         // ------------------------------------------------------------ producer
         if (lane == 0) {
@@ -417,6 +423,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     } else {
         regs_inc<RADIAL_FWD_REGS_HI>();
+        FWD_WORK_ITEM;
         // ------------------------------------------------------------ softmax
         const int t = (warp - 4) >> 2;                 // Q tile
         const int r = ((warp & 3) << 5) + lane;        // row in tile = TMEM lane
@@ -507,7 +514,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                 // (i, k) in each key frame j the block overlaps (mask.hpp:238-272).  K1 flags the
                 // entries whose whole tile keeps the whole block (ufull): those take the
                 // block path's unmasked code with no per-row mask.
+#ifdef RADIAL_TOK_NOMASK
+                const bool tile_full = true;  // timing hook: token kernel without any masking work
+#else
                 const bool tile_full = (__ldg(p.ufull + ebase + j) >> t) & 1u;
+#endif
 #pragma unroll
                 for (int w = 0; w < BK / 32; ++w) {
                     const int len = min(max(valid - 32 * w, 0), 32);
@@ -574,7 +585,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                 bool all = true;
 #pragma unroll
                 for (int w = 0; w < BK / 32; ++w) all = all && kmask[w] == 0xffffffffu;
+#ifdef RADIAL_TOK_NOSELECT
+                full = active && (all || kmask[0] != 1u);  // timing hook: build masks, skip applying them
+#else
                 full = active && all;
+#endif
             }
             if (!full) {
                 // rare (tail KV block, a row whose query block skips J, or a token-masked
@@ -718,6 +733,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     if (threadIdx.x == 0) TRACE(22, 1);  // CTA end
 }
+#undef FWD_WORK_ITEM
 
 using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
                                    const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,

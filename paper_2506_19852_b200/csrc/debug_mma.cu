@@ -637,17 +637,18 @@ extern "C" int radial_cuda_debug_red_rate(int mode, float* buf, uint32_t blocks,
 // The smallest instance of K3's lse2 / D staging: lane 0 of warp 0 bulk-copies 512 B into
 // shared memory (completion on an mbarrier), warp 1 waits on that mbarrier and reads the
 // bytes; then a second round re-fills the same buffer after warp 1 has released it through a
-// second mbarrier (fence.proxy.async first), as the dK/dV ring does.  Correct by the
-// mbarrier / async-proxy rules; run under compute-sanitizer --tool racecheck to see whether
-// the tool reports it (scripts/racecheck_probe.py).
+// second mbarrier (fence.proxy.async first), as the dK/dV ring does.  Release mode 0: every
+// lane arrives (count 32); mode 1: __syncwarp, then lane 0 arrives for the warp (count 1, the
+// pattern the kernels use).  Both are correct under the PTX memory model; run under
+// compute-sanitizer --tool racecheck to see which the tool accepts (scripts/racecheck_probe.py).
 namespace {
-__global__ void racecheck_probe_kernel(const float* src, float* out) {
+__global__ void racecheck_probe_kernel(const float* src, float* out, int mode) {
     __shared__ alignas(128) float buf[128];
     __shared__ alignas(8) uint64_t full, empty;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
         mbar_init(&full, 1);
-        mbar_init(&empty, 32);
+        mbar_init(&empty, mode ? 1 : 32);
         fence_barrier_init();
     }
     __syncthreads();
@@ -662,14 +663,19 @@ __global__ void racecheck_probe_kernel(const float* src, float* out) {
             for (int x = 0; x < 4; ++x) acc += buf[lane * 4 + x];
             out[round * 32 + lane] = acc;
             fence_proxy_async_smem();
-            mbar_arrive(&empty);
+            if (mode) {
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&empty);
+            } else {
+                mbar_arrive(&empty);
+            }
         }
     }
 }
 }  // namespace
 
-extern "C" int radial_cuda_debug_racecheck_probe(const float* src, float* out) {
-    racecheck_probe_kernel<<<1, 64>>>(src, out);
+extern "C" int radial_cuda_debug_racecheck_probe(const float* src, float* out, int mode) {
+    racecheck_probe_kernel<<<1, 64>>>(src, out, mode);
     RADIAL_CUDA_TRY(cudaGetLastError());
     RADIAL_CUDA_TRY(cudaDeviceSynchronize());
     return RADIAL_OK;

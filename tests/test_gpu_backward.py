@@ -12,8 +12,10 @@ from tests._util import bf16_pipeline_bwd, instance_bf16, to_torch_bf16
 
 pytestmark = pytest.mark.gpu
 
-BWD_REL_L2 = 2e-2   # per block; bf16 P/dS operands with fp32 accumulation
-BWD_GLOBAL = 1e-2   # whole tensor
+# bf16 P / dS MMA operands with fp32 accumulation.  Measured on B200: ~2.4e-3 per block and
+# globally at d = 128, against a bf16-pipeline floor of ~1.7e-3 (test_backward_error_near_bf16_floor)
+BWD_REL_L2 = 1e-2   # per block (the forward's rel-L2 gate)
+BWD_GLOBAL = 6e-3   # whole tensor
 
 
 @pytest.fixture(scope="module")
