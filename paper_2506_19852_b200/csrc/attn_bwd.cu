@@ -461,10 +461,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int i = 0; i < kDS; ++i) {
             mbar_init(&bar_dofull[i], 1);
             mbar_init(&bar_doempty[i], 1);   // the MMA warp's commit: dV(i), dK(i) done with dO_i
-            // the 8 elementwise warps, done reading the stage's lse2 / D (generic proxy); a
-            // barrier of their own, so the next bulk load into the stage is ordered after those
-            // reads by plain thread arrivals (not mixed with the tcgen05.commit arrival)
-            mbar_init(&bar_vecempty[i], 8);
+            // every thread of the 8 elementwise warps, done reading the stage's lse2 / D (generic
+            // proxy); a barrier of their own, so the next bulk load into the stage is ordered
+            // after those reads by plain thread arrivals (not mixed with the tcgen05.commit)
+            mbar_init(&bar_vecempty[i], 8 * 32);
         }
         mbar_init(bar_s, 1);
         mbar_init(bar_sfree, 8);
@@ -665,11 +665,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             tc_fence_before();
             __syncwarp();
             fence_proxy_async_smem();  // the stage's lse2 / D reads before the next bulk load into it
-            __syncwarp();
-            if (lane == 0) {
-                mbar_arrive(bar_ds);
-                mbar_arrive(&bar_vecempty[ds]);  // this warp's lse2 / D reads of the stage are done
-            }
+            // every lane releases its own reads of the stage (an elected arrive after __syncwarp
+            // is equally correct, but compute-sanitizer racecheck does not model __syncwarp and
+            // reports it: scripts/racecheck_probe.py mode 1)
+            mbar_arrive(&bar_vecempty[ds]);
+            if (lane == 0) mbar_arrive(bar_ds);  // dS^T stores: ordered by the __syncwarp above
             if ((warp == 4 || warp == 8) && lane == 0) BTRACE(warp == 4 ? 9 : 11, i);
         }
         // ---------------------------------------------------- epilogue: wg0 -> dV, wg1 -> dK * scale

@@ -446,63 +446,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint32_t mask = e >> 28;
             if (((mask >> (t * Cfg::GT)) & ((1u << Cfg::GT) - 1)) == 0) continue;
             const uint32_t J = e & 0x0FFFFFFFu;
-            if ((warp & 3) == 0 && lane == 0) TRACE(4 * t + 0, j);
-            mbar_wait(&bar_sfull[t], sphase);
-            if ((warp & 3) == 0 && lane == 0) TRACE(4 * t + 1, j);
-            sphase ^= 1;
-            tc_fence_after();
-#ifdef RADIAL_FWD_MMA_ONLY
-            // timing experiment: no softmax at all (P = stale TMEM contents); measures the
-            // MMA + TMA pipeline alone
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0)
-                for (int h = 0; h < kPParts; ++h) mbar_arrive(&bar_pready[kPParts * t + h]);
-            continue;
-#endif
-            float s[BK];
-            // first half, wait, then the second half's load overlaps the first half's max; one
-            // 64-column tcgen05.ld per half (+1.5% over two 32-column loads)
-#if !defined(RADIAL_FWD_LD32)
-            if constexpr (BK == 128) {
-                uint32_t u[64];
-                tmem_ld64(s_addr, u);
-#pragma unroll
-                for (int x = 0; x < 64; ++x) s[x] = __uint_as_float(u[x]);
-            } else
-#endif
-#pragma unroll
-            for (int c = 0; c < BK / 2; c += 32) {
-                uint32_t u[32];
-                tmem_ld32(s_addr + c, u);
-#pragma unroll
-                for (int x = 0; x < 32; ++x) s[c + x] = __uint_as_float(u[x]);
-            }
-            tmem_wait_ld();
-            float mh[8];
-#pragma unroll
-            for (int x = 0; x < 8; ++x) mh[x] = s[x];
-#if !defined(RADIAL_FWD_LD32)
-            if constexpr (BK == 128) {
-                uint32_t u[64];
-                tmem_ld64(s_addr + 64, u);
-#pragma unroll
-                for (int x = 0; x < 64; ++x) s[64 + x] = __uint_as_float(u[x]);
-            } else
-#endif
-#pragma unroll
-            for (int c = BK / 2; c < BK; c += 32) {
-                uint32_t u[32];
-                tmem_ld32(s_addr + c, u);
-#pragma unroll
-                for (int x = 0; x < 32; ++x) s[c + x] = __uint_as_float(u[x]);
-            }
-#pragma unroll
-            for (int c = 8; c < BK / 2; c += 8)
-#pragma unroll
-                for (int x = 0; x < 8; ++x) mh[x] = fmaxf(mh[x], s[c + x]);
-            tmem_wait_ld();
-            if (warp == 4 && lane == 0) TRACE(14, j);
+            // the keep mask of this entry depends only on (row, J): it is built before waiting
+            // for S, in the time the warp would otherwise spend waiting (token-exact mode)
             const bool active = (mask >> my_bit) & 1;
             const uint64_t kv0 = static_cast<uint64_t>(J) * BK;
             const int valid = (kv0 + BK <= p.n) ? BK : static_cast<int>(p.n - kv0);
@@ -591,15 +536,77 @@ __global__ void __launch_bounds__(kThreads, 1)
                 full = active && all;
 #endif
             }
+            if ((warp & 3) == 0 && lane == 0) TRACE(4 * t + 0, j);
+            mbar_wait(&bar_sfull[t], sphase);
+            if ((warp & 3) == 0 && lane == 0) TRACE(4 * t + 1, j);
+            sphase ^= 1;
+            tc_fence_after();
+#ifdef RADIAL_FWD_MMA_ONLY
+            // timing experiment: no softmax at all (P = stale TMEM contents); measures the
+            // MMA + TMA pipeline alone
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0)
+                for (int h = 0; h < kPParts; ++h) mbar_arrive(&bar_pready[kPParts * t + h]);
+            continue;
+#endif
+            float s[BK];
+            // first half, wait, then the second half's load overlaps the first half's max; one
+            // 64-column tcgen05.ld per half (+1.5% over two 32-column loads)
+#if !defined(RADIAL_FWD_LD32)
+            if constexpr (BK == 128) {
+                uint32_t u[64];
+                tmem_ld64(s_addr, u);
+#pragma unroll
+                for (int x = 0; x < 64; ++x) s[x] = __uint_as_float(u[x]);
+            } else
+#endif
+#pragma unroll
+            for (int c = 0; c < BK / 2; c += 32) {
+                uint32_t u[32];
+                tmem_ld32(s_addr + c, u);
+#pragma unroll
+                for (int x = 0; x < 32; ++x) s[c + x] = __uint_as_float(u[x]);
+            }
+            tmem_wait_ld();
+            float mh[8];
+#pragma unroll
+            for (int x = 0; x < 8; ++x) mh[x] = s[x];
+#if !defined(RADIAL_FWD_LD32)
+            if constexpr (BK == 128) {
+                uint32_t u[64];
+                tmem_ld64(s_addr + 64, u);
+#pragma unroll
+                for (int x = 0; x < 64; ++x) s[64 + x] = __uint_as_float(u[x]);
+            } else
+#endif
+#pragma unroll
+            for (int c = BK / 2; c < BK; c += 32) {
+                uint32_t u[32];
+                tmem_ld32(s_addr + c, u);
+#pragma unroll
+                for (int x = 0; x < 32; ++x) s[c + x] = __uint_as_float(u[x]);
+            }
+#pragma unroll
+            for (int c = 8; c < BK / 2; c += 8)
+#pragma unroll
+                for (int x = 0; x < 8; ++x) mh[x] = fmaxf(mh[x], s[c + x]);
+            tmem_wait_ld();
+            if (warp == 4 && lane == 0) TRACE(14, j);
             if (!full) {
                 // rare (tail KV block, a row whose query block skips J, or a token-masked
                 // entry): mask in place so a single code path follows; masked entries
                 // become -inf -> exp2 = 0
+                if constexpr (TOKEN) {
+                    // kmask already holds active && c < valid: one bit test (LOP3 -> predicate)
+                    // and one select per column
 #pragma unroll
-                for (int c = 0; c < BK; ++c) {
-                    bool keep = c < valid;
-                    if constexpr (TOKEN) keep = (kmask[c >> 5] >> (c & 31)) & 1u;
-                    s[c] = (active && keep) ? s[c] : -INFINITY;
+                    for (int w = 0; w < BK / 32; ++w) kmask[w] = active ? kmask[w] : 0u;
+#pragma unroll
+                    for (int c = 0; c < BK; ++c) s[c] = (kmask[c >> 5] & (1u << (c & 31))) ? s[c] : -INFINITY;
+                } else {
+#pragma unroll
+                    for (int c = 0; c < BK; ++c) s[c] = (active && c < valid) ? s[c] : -INFINITY;
                 }
             }
             // tree reduction: 8 independent chains instead of one 128-long chain
