@@ -100,6 +100,13 @@ constexpr int kPolyPairs = RADIAL_POLY_PAIRS;  // column pairs per 8 using the p
 
 constexpr int kMaxDst = 8;  // fused all-gather: O rows stored into up to 8 ranks' buffers
 
+#ifndef RADIAL_TOK_PAIRED
+#define RADIAL_TOK_PAIRED 0
+#endif
+// token-exact mode over the paired work lists with the early S issue (as the block path)
+// instead of the ascending lists
+constexpr bool kTokPaired = RADIAL_TOK_PAIRED != 0;
+
 struct FwdParams {
     __nv_bfloat16* o;
     float* lse;
@@ -306,7 +313,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     // softmaxes overlap as in a shared step
                     // (block layouts only: the token-exact path keeps ascending lists, whose
                     // solo entries are rarely adjacent, and measured 4% slower with this logic)
-                    if (!TOKEN && tf0 && !tf1 && j + 1 < L) {
+                    if ((!TOKEN || kTokPaired) && tf0 && !tf1 && j + 1 < L) {
                         const uint32_t mn = e_next >> 28;
                         early = !(mn & ((1u << Cfg::GT) - 1)) && ((mn >> Cfg::GT) & ((1u << Cfg::GT) - 1));
                     }
@@ -401,7 +408,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     pv1_step = j + 1;
                 }
                 b_done = false;
-                if (!TOKEN && early) {
+                if ((!TOKEN || kTokPaired) && early) {
                     constexpr int KSL1 = (2 * PH + 2) % kSlots;  // slot of K_{j+1}
                     mbar_wait(&bar_full[KSL1], ((2 * j + 2) / kSlots) & 1);
                     tc_fence_after();
@@ -812,7 +819,7 @@ int launch_fwd_t(const void* q, const void* k, const void* v, void* o, float* ls
     p.dense = L == nullptr;
     if (L) {
         p.uptr = L->uptr;
-        p.uidx = (token && L->uidx_asc) ? L->uidx_asc : L->uidx;
+        p.uidx = (token && !kTokPaired && L->uidx_asc) ? L->uidx_asc : L->uidx;
 #ifndef RADIAL_FWD_NATURAL_ORDER
         p.order = L->uorder;
 #endif

@@ -23,6 +23,10 @@
 #include "mask_rule.cuh"
 #include "radial_internal.h"
 
+#ifndef RADIAL_TOK_PAIRED
+#define RADIAL_TOK_PAIRED 0  // token-exact flags over the paired lists (attn_fwd.cu kTokPaired)
+#endif
+
 namespace {
 
 using radial_rule::MaskParams;
@@ -542,7 +546,7 @@ int build_worklists(radial_layout* L, cudaStream_t st) {
             const MaskParams mp{L->f, L->s, L->B, static_cast<uint64_t>(L->f) * L->s, L->kind, L->sink, L->tw, L->sw};
             RADIAL_CUDA_TRY(cudaMallocAsync(&L->ufull, un, st));
             token_full_flags<<<(C + warps_per_cta - 1) / warps_per_cta, 32 * warps_per_cta, 0, st>>>(
-                mp, L->uptr, C, L->G, L->uidx_asc, L->ufull);
+                mp, L->uptr, C, L->G, RADIAL_TOK_PAIRED ? L->uidx : L->uidx_asc, L->ufull);
             RADIAL_CUDA_TRY(cudaGetLastError());
             count_launches(1);
         }
