@@ -307,6 +307,7 @@ const char* radial_cuda_last_error(void) { return g_last_error.c_str(); }
 int radial_cuda_mask_build(uint32_t frames, uint32_t tokens_per_frame, uint32_t block_size, int kind,
                            int sink, uint32_t temporal_window, uint32_t spatial_window, void* stream,
                            radial_layout** out) {
+    RADIAL_NVTX("radial_cuda_mask_build");
     if (!out) return fail(RADIAL_ERR_INVALID, "null output handle");
     *out = nullptr;
     int rc = check_shape(frames, tokens_per_frame, block_size);
@@ -335,6 +336,7 @@ int radial_cuda_mask_build(uint32_t frames, uint32_t tokens_per_frame, uint32_t 
 int radial_cuda_layout_from_csr(uint32_t frames, uint32_t tokens_per_frame, uint32_t block_size,
                                 int kind, int sink, uint32_t grid_rows, const uint64_t* row_ptr,
                                 const uint32_t* col_idx, void* stream, radial_layout** out) {
+    RADIAL_NVTX("radial_cuda_layout_from_csr");
     if (!out || !row_ptr) return fail(RADIAL_ERR_INVALID, "null argument");
     *out = nullptr;
     int rc = check_shape(frames, tokens_per_frame, block_size);
@@ -586,6 +588,7 @@ void radial_cuda_layout_free(radial_layout* L) { free_layout(L); }
 int radial_cuda_attn_fwd(const void* q, const void* k, const void* v, void* o, float* lse,
                          uint32_t heads, uint64_t n, uint32_t head_dim, float scale,
                          const radial_layout* layout, void* stream) {
+    RADIAL_NVTX("radial_cuda_attn_fwd");
     int rc = check_attn(q, k, v, o, heads, n, head_dim);
     if (rc) return rc;
     if ((rc = check_layout_for_attn(layout, n))) return rc;
@@ -597,6 +600,7 @@ int radial_cuda_attn_fwd_scatter(const void* q, const void* k, const void* v, vo
                                  uint32_t n_dst, uint32_t head_base, uint32_t heads_full, float* lse,
                                  uint32_t heads, uint64_t n, uint32_t head_dim, float scale,
                                  const radial_layout* layout, void* stream) {
+    RADIAL_NVTX("radial_cuda_attn_fwd_scatter");
     if (!o_dst || n_dst < 1 || n_dst > 8)
         return fail(RADIAL_ERR_INVALID, "attn_fwd_scatter: 1..8 destination buffers");
     for (uint32_t r = 0; r < n_dst; ++r)
@@ -618,6 +622,7 @@ int radial_cuda_attn_fwd_scatter(const void* q, const void* k, const void* v, vo
 int radial_cuda_attn_fwd_token(const void* q, const void* k, const void* v, void* o, float* lse,
                                uint32_t heads, uint64_t n, uint32_t head_dim, float scale,
                                const radial_layout* layout, void* stream) {
+    RADIAL_NVTX("radial_cuda_attn_fwd_token");
     int rc = check_attn(q, k, v, o, heads, n, head_dim);
     if (rc) return rc;
     if ((rc = check_layout_for_attn(layout, n))) return rc;
@@ -630,6 +635,7 @@ int radial_cuda_attn_fwd_token(const void* q, const void* k, const void* v, void
 int radial_cuda_attn_fwd_dense(const void* q, const void* k, const void* v, void* o, float* lse,
                                uint32_t heads, uint64_t n, uint32_t head_dim, uint32_t block_size,
                                float scale, void* stream) {
+    RADIAL_NVTX("radial_cuda_attn_fwd_dense");
     int rc = check_attn(q, k, v, o, heads, n, head_dim);
     if (rc) return rc;
     if (block_size != 64 && block_size != 128)
@@ -641,6 +647,7 @@ int radial_cuda_attn_fwd_dense(const void* q, const void* k, const void* v, void
 int radial_cuda_attn_fwd_host(const void* q, const void* k, const void* v, void* o, float* lse,
                               uint32_t heads, uint64_t n, uint32_t head_dim, float scale,
                               const radial_layout* layout, void* stream) {
+    RADIAL_NVTX("radial_cuda_attn_fwd_host");
     int rc = check_attn(q, k, v, o, heads, n, head_dim);
     if (rc) return rc;
     if ((rc = check_layout_for_attn(layout, n))) return rc;
@@ -653,6 +660,7 @@ int radial_cuda_attn_fwd_host_multi(const void* q, const void* k, const void* v,
                                     uint32_t frames, uint32_t tokens_per_frame, uint32_t block_size, int kind,
                                     int sink, uint32_t temporal_window, uint32_t spatial_window,
                                     const int* devices, int num_devices) {
+    RADIAL_NVTX("radial_cuda_attn_fwd_host_multi");
     if (!devices || num_devices < 1) return fail(RADIAL_ERR_INVALID, "attn_fwd_host_multi: no devices");
     int rc = check_attn(q, k, v, o, heads, n, head_dim);
     if (rc) return rc;
@@ -702,6 +710,7 @@ int radial_cuda_attn_fwd_host_multi(const void* q, const void* k, const void* v,
 int radial_cuda_attn_fwd_token_host(const void* q, const void* k, const void* v, void* o, float* lse,
                                     uint32_t heads, uint64_t n, uint32_t head_dim, float scale,
                                     const radial_layout* layout, void* stream) {
+    RADIAL_NVTX("radial_cuda_attn_fwd_token_host");
     int rc = check_attn(q, k, v, o, heads, n, head_dim);
     if (rc) return rc;
     if ((rc = check_layout_for_attn(layout, n))) return rc;
@@ -714,6 +723,7 @@ int radial_cuda_attn_fwd_token_host(const void* q, const void* k, const void* v,
 int radial_cuda_attn_fwd_dense_host(const void* q, const void* k, const void* v, void* o, float* lse,
                                     uint32_t heads, uint64_t n, uint32_t head_dim, uint32_t block_size,
                                     float scale, void* stream) {
+    RADIAL_NVTX("radial_cuda_attn_fwd_dense_host");
     int rc = check_attn(q, k, v, o, heads, n, head_dim);
     if (rc) return rc;
     if (block_size != 64 && block_size != 128)
@@ -730,6 +740,7 @@ int radial_cuda_attn_bwd(const void* q, const void* k, const void* v, const void
                          const void* dout, void* dq, void* dk, void* dv, uint32_t heads, uint64_t n,
                          uint32_t head_dim, float scale, const radial_layout* layout, void* workspace,
                          void* stream) {
+    RADIAL_NVTX("radial_cuda_attn_bwd");
     int rc = check_attn(q, k, v, o, heads, n, head_dim);
     if (rc) return rc;
     if (!lse || !dout || !dq || !dk || !dv) return fail(RADIAL_ERR_INVALID, "attn_bwd: null tensor");

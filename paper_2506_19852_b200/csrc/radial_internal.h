@@ -88,3 +88,22 @@ int build_worklists(radial_layout* L, cudaStream_t st);
         cudaError_t e_ = (expr);                                                \
         if (e_ != cudaSuccess) return radial_detail::cuda_fail(e_, #expr);      \
     } while (0)
+
+// NVTX ranges around every C-ABI entry point that launches work (nsys / ncu --nvtx see the
+// reference-facing call boundaries); NVTX v3 is header-only and a no-op without a tool.
+#ifndef RADIAL_NO_NVTX
+#include <nvtx3/nvToolsExt.h>
+namespace radial_detail {
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
+};
+}  // namespace radial_detail
+#define RADIAL_NVTX(name) radial_detail::NvtxRange radial_nvtx_range_(name)
+#else
+#define RADIAL_NVTX(name) \
+    do {                  \
+    } while (0)
+#endif
