@@ -386,8 +386,9 @@ def run_ours(args, world, rank, local):
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
             tj = json.load(fh)
-        traffic = tj.get(args.config)
-        traffic_src = tj.get("_source")
+        if world == 1 or args.weak:  # the capture is of the whole 24-head launch
+            traffic = tj.get(args.config)
+            traffic_src = tj.get("_source") if traffic is not None else None
     except Exception:
         pass
     line = {

@@ -484,9 +484,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                     auto set = [&](uint64_t v) {
                         if (v < v0 || v - v0 >= vn) return;
                         const uint32_t c = static_cast<uint32_t>(v - v0);
+                        // branch-free per-word update: a data-dependent word index would put
+                        // kmask in local memory for the whole loop
 #pragma unroll
                         for (int w = 0; w < BK / 32; ++w)
-                            if ((c >> 5) == static_cast<uint32_t>(w)) kmask[w] |= 1u << (c & 31);
+                            kmask[w] |= (1u << (c & 31)) & (0u - static_cast<uint32_t>((c >> 5) == static_cast<uint32_t>(w)));
                     };
                     if (p.rule.sink && v0 < p.rule.s) {
                         const uint32_t hi = static_cast<uint32_t>(min(static_cast<uint64_t>(p.rule.s) - v0, vn));

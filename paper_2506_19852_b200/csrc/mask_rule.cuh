@@ -48,9 +48,16 @@ __host__ __device__ __forceinline__ bool kept_span(const MaskParams& p, uint32_t
             hi = s - 1;
             return true;
         case RADIAL_KIND_RADIAL: {
-            const uint32_t e = d <= 1 ? 0u : floor_log2_u64(d);
+            // frame distances are < 2^32: the band test in 32-bit arithmetic (the token-exact
+            // forward evaluates this per row and block)
+            const uint32_t d32 = static_cast<uint32_t>(d);
+#ifdef __CUDA_ARCH__
+            const uint32_t e = d32 <= 1 ? 0u : 31u - static_cast<uint32_t>(__clz(static_cast<int>(d32)));
+#else
+            const uint32_t e = d32 <= 1 ? 0u : 31u - static_cast<uint32_t>(__builtin_clz(d32));
+#endif
+            if ((1u << e) <= s) return band((s >> e) - 1);  // s / 2^e
             const uint64_t pw = 1ull << e;
-            if (pw <= s) return band((s >> e) - 1);  // s / 2^e (e < 32 here)
             const uint64_t period = (pw + s - 1) / s;
             if (d % period == 0) {
                 lo = k_lo;
