@@ -124,6 +124,7 @@ struct FwdParams {
     float scale_log2;
     int dense;
     radial_rule::MaskParams rule;  // token-exact mode: the pattern's keep rule
+    uint32_t s_inv;                // token-exact mode: floor((2^32 - 1) / s), for key frame = key / s
 };
 
 template <int D, int BK>
@@ -442,7 +443,6 @@ __global__ void __launch_bounds__(kThreads, 1)
         // token coordinates (frame, position) of this row, for the token-exact mode
         const uint32_t tok_i = TOKEN ? static_cast<uint32_t>(grow / p.rule.s) : 0u;
         const uint32_t tok_k = TOKEN ? static_cast<uint32_t>(grow % p.rule.s) : 0u;
-        uint32_t tok_jf = 0, tok_fs = 0;  // token mode: key frame (and its first key) of the current block
         const float sl2 = p.scale_log2;
         float m = -INFINITY, l = 0.f;
         uint32_t sphase = 0;
@@ -508,18 +508,15 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                 } else if (active && grow < p.n) {
                     const uint32_t v0 = J * BK, v1 = v0 + static_cast<uint32_t>(valid) - 1;
-                    // key frame of the block's first key, tracked incrementally (the KV list is
-                    // ascending) instead of a division per block
-                    if (v0 < tok_fs) {
-                        tok_jf = v0 / p.rule.s;
-                        tok_fs = tok_jf * p.rule.s;
+                    // key frame of the block's first key: v0 / s through the host-computed
+                    // reciprocal (an under-estimate by at most 2, fixed up), any list order
+                    uint32_t jf0 = __umulhi(v0, p.s_inv), fs0 = jf0 * p.rule.s;
+                    while (fs0 + p.rule.s <= v0) {
+                        ++jf0;
+                        fs0 += p.rule.s;
                     }
-                    while (tok_fs + p.rule.s <= v0) {
-                        ++tok_jf;
-                        tok_fs += p.rule.s;
-                    }
-                    uint32_t fs = tok_fs;
-                    for (uint32_t jf = tok_jf; fs <= v1; ++jf, fs += p.rule.s) {
+                    uint32_t fs = fs0;
+                    for (uint32_t jf = jf0; fs <= v1; ++jf, fs += p.rule.s) {
                         uint32_t lo, hi;
                         if (!radial_rule::kept_span(p.rule, tok_i, tok_k, tok_k, jf, lo, hi)) continue;
                         const uint32_t a = max(fs + lo, v0) - v0;
@@ -828,6 +825,7 @@ int launch_fwd_t(const void* q, const void* k, const void* v, void* o, float* ls
     }
     if (token) {
         p.rule = radial_rule::MaskParams{L->f, L->s, L->B, n, L->kind, L->sink, L->tw, L->sw};
+        p.s_inv = 0xffffffffu / L->s;
         p.ufull = L->ufull;
         if (!p.ufull) return fail(RADIAL_ERR_INVALID, "masked_attention: token-exact mode needs a layout built by radial_cuda_mask_build");
     }

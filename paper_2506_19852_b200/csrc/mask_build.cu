@@ -425,7 +425,10 @@ int lpt_order(const uint64_t* dptr, uint32_t n, cudaStream_t st, uint32_t** orde
     int dev = 0, sms = 148;
     RADIAL_CUDA_TRY(cudaGetDevice(&dev));
     RADIAL_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    const uint32_t window = 2u * static_cast<uint32_t>(std::max(sms, 1));
+#ifndef RADIAL_LPT_WINDOW_SMS
+#define RADIAL_LPT_WINDOW_SMS 2  // window = this many x the SM count (tuning knob)
+#endif
+    const uint32_t window = RADIAL_LPT_WINDOW_SMS * static_cast<uint32_t>(std::max(sms, 1));
     if (n <= static_cast<uint32_t>(kSortMax)) {
         lpt_sort_kernel<<<1, 1024, 0, st>>>(dptr, n, window, *order_out);
         RADIAL_CUDA_TRY(cudaGetLastError());
