@@ -35,8 +35,8 @@
 // setmaxnreg split: producer/MMA warpgroup vs elementwise warpgroups (384 threads x 168 =
 // 128 x LO + 256 x HI must hold)
 #ifndef RADIAL_FWD_REGS_LO
-#define RADIAL_FWD_REGS_LO 72
-#define RADIAL_FWD_REGS_HI 216
+#define RADIAL_FWD_REGS_LO 40   // the producer / MMA warps issue from uniform registers
+#define RADIAL_FWD_REGS_HI 232  // 128 x 40 + 256 x 232 = 384 x 168: no spills in any instantiation
 #endif
 
 using namespace radial_sm100;
@@ -231,7 +231,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     constexpr uint32_t tmem = kTmem;
     // producer / MMA / allocator warpgroup needs few registers (the grouped MMA issue keeps
     // its operands in uniform registers); the two softmax warpgroups hold a 128-column S row
-    // each (128 x 72 + 256 x 216 <= 64K; measured +1% over 104 / 200, no spills)
+    // each (128 x LO + 256 x HI = 384 x 168, the launch allocation; 72 / 216 was +1% over
+    // 104 / 200, and 40 / 232 removes the last spills)
     if (warp < 4) {
         regs_dec<RADIAL_FWD_REGS_LO>();
         FWD_WORK_ITEM;
