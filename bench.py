@@ -129,7 +129,7 @@ def spawn_ranks(args) -> int:
     """`--gpus N` without a torchrun environment: re-launch this script under
     torch.distributed.run with N ranks on this node (the driver's command shape)."""
     import subprocess
-    if not args.dry_run:
+    if not args.dry_run and not args.shared_gpu:
         try:
             import torch
             have = torch.cuda.device_count()
@@ -426,6 +426,9 @@ def run_ours(args, world, rank, local):
         "gpu_launches_source": "radial_cuda_kernel_launches() delta over the timed region (this library's kernels)",
         "clocks": clk.summary(),
     }
+    if args.shared_gpu and world > 1:
+        line["shared_gpu_plumbing_test"] = ("all ranks ran on cuda:0 with gloo collectives: the N > 1 code path "
+                                            "end to end, not a multi-GPU measurement")
     print(json.dumps(line))
 
 
@@ -609,6 +612,10 @@ def main():
                          "epilogue stores each row into every rank's buffer over peer memory")
     ap.add_argument("--gather-nccl", action="store_true",
                     help="with --gather: NCCL all-gather after the kernel instead (comparison)")
+    ap.add_argument("--shared-gpu", action="store_true",
+                    help="plumbing test for boxes with one GPU: every rank runs on cuda:0 with gloo "
+                         "collectives (no reassembly timings); the line is marked and its timings are not "
+                         "a multi-GPU measurement")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -620,7 +627,12 @@ def main():
         return
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         sys.exit(spawn_ranks(args))
-    world, rank, local = dist_setup("gloo" if args.dry_run else "nccl")
+    world, rank, local = dist_setup("gloo" if (args.dry_run or args.shared_gpu) else "nccl")
+    if args.shared_gpu and not args.dry_run:
+        import torch
+        torch.cuda.set_device(0)
+        local = 0
+        args.no_gather = True
     if world != args.gpus:
         print(f"bench.py: --gpus {args.gpus} but the launch has WORLD_SIZE={world}", file=sys.stderr)
         sys.exit(2)
