@@ -95,3 +95,24 @@ def test_bench_rejects_world_size_mismatch():
     r = _bench(["--gpus", "2", "--dry-run"], {"WORLD_SIZE": "1", "RANK": "0", "LOCAL_RANK": "0"})
     assert r.returncode == 2
     assert "WORLD_SIZE=1" in r.stderr
+
+
+def test_bench_refuses_more_gpus_than_visible_without_shared_flag():
+    """`--gpus N` on a box with fewer devices fails loudly (exit 2) instead of running all heads
+    on one GPU; here (no GPU at all) any N > 0 is more than visible."""
+    r = _bench(["--gpus", "2"])
+    assert r.returncode == 2
+    assert "CUDA device(s) visible" in r.stderr
+
+
+@pytest.mark.gpu
+def test_bench_shared_gpu_runs_the_multi_rank_path():
+    """Two ranks on the one GPU of a gpurun box (gloo collectives): the whole N > 1 bench path
+    completes and the line is marked as a plumbing test."""
+    import json
+    r = _bench(["--gpus", "2", "--shared-gpu", "--steps", "2", "--warmup", "3", "--no-cpu-baseline",
+                "--no-extra", "--no-bwd", "--no-dense"])
+    assert r.returncode == 0, r.stderr[-3000:]
+    line = json.loads(r.stdout.strip().splitlines()[-1])
+    assert line["n_gpus"] == 2 and line["config"]["heads_per_rank"] == [[0, 12], [12, 24]]
+    assert "shared_gpu_plumbing_test" in line and line["gpu_launches"] >= 4
