@@ -185,3 +185,113 @@ def test_dense_comparator_hunyuan33_sampled(P):
         rows_ok = ((blocks[:, None] * B + torch.arange(B, device="cuda")) < n).reshape(-1, 1)
         mx, rel = _per_block_errors(got * rows_ok, want * rows_ok, B)
         assert float(mx.max()) <= MAX_ABS and float(rel.max()) <= REL_L2, (h, float(mx.max()), float(rel.max()))
+
+
+# ------------------------------------------------------------------------------ backward
+def fp32_blockwise_bwd(q, k, v, do, idx, lens, B, n, scale):
+    """fp32 restatement of the K3 gradients for one head over the kept blocks (no reference
+    exists): P = exp(S - lse), dV = P^T dO, dP = dO V^T, D = rowsum(dO o O),
+    dS = P o (dP - D), dQ = scale dS K, dK = scale dS^T Q.  q/k/v/do bf16 [n, d] on the GPU;
+    returns fp32 dq, dk, dv [R * B, d] (rows >= n are zero)."""
+    import torch
+    R = idx.shape[0]
+    d = q.shape[1]
+    o, lse = fp32_blockwise(q, k, v, idx, lens, B, n, scale)
+    pad = R * B + B - n
+    qf = torch.nn.functional.pad(q.float(), (0, 0, 0, pad)).view(R + 1, B, d)
+    kf = torch.nn.functional.pad(k.float(), (0, 0, 0, pad)).view(R + 1, B, d)
+    vf = torch.nn.functional.pad(v.float(), (0, 0, 0, pad)).view(R + 1, B, d)
+    dof = torch.nn.functional.pad(do.float(), (0, 0, 0, pad)).view(R + 1, B, d)
+    lsef = torch.nn.functional.pad(lse, (0, B)).view(R + 1, B)
+    valid = (torch.arange((R + 1) * B, device=q.device) < n).view(R + 1, B)
+    dvec = (dof[:R] * o.view(R, B, d)).sum(-1) * valid[:R]
+    dq = torch.zeros(R, B, d, device=q.device)
+    dk = torch.zeros(R + 1, B, d, device=q.device)
+    dv = torch.zeros(R + 1, B, d, device=q.device)
+    Lmax = idx.shape[1]
+    nb = max(1, int(2 ** 28 // (Lmax * B * B * 4)))
+    ar = torch.arange(B, device=q.device)
+    for b0 in range(0, R, nb):
+        bl = torch.arange(b0, min(R, b0 + nb), device=q.device)
+        L = int(lens[bl].max().item())
+        ib = idx[bl, :L]                                              # [nb, L]
+        kg = kf[ib].reshape(bl.numel(), L * B, d)
+        vg = vf[ib].reshape(bl.numel(), L * B, d)
+        key = (ib[:, :, None] * B + ar).reshape(bl.numel(), 1, L * B)
+        ok = (ib[:, :, None] < R).expand(-1, -1, B).reshape(bl.numel(), 1, L * B) & (key < n) & valid[bl][:, :, None]
+        s = torch.bmm(qf[bl], kg.transpose(1, 2)) * scale
+        p = torch.exp(s - lsef[bl][:, :, None]).masked_fill(~ok, 0.0)      # [nb, B, L*B]
+        dp = torch.bmm(dof[bl], vg.transpose(1, 2))
+        ds = p * (dp - dvec[bl][:, :, None])
+        dq[bl] = torch.bmm(ds, kg) * scale
+        # per kept (I, J): dK_J += dS_IJ^T Q_I, dV_J += P_IJ^T dO_I
+        ds4 = ds.view(bl.numel(), B, L, B)
+        p4 = p.view(bl.numel(), B, L, B)
+        dkc = torch.einsum("nilj,nid->nljd", ds4, qf[bl]) * scale        # [nb, L, B, d]
+        dvc = torch.einsum("nilj,nid->nljd", p4, dof[bl])
+        dk.index_add_(0, ib.reshape(-1), dkc.reshape(-1, B, d))
+        dv.index_add_(0, ib.reshape(-1), dvc.reshape(-1, B, d))
+    return dq.reshape(-1, d), dk[:R].reshape(-1, d), dv[:R].reshape(-1, d)
+
+
+def test_backward_restatement_matches_fp64_oracle(P):
+    """The fp32 backward restatement equals the fp64 oracle (oracle.attention_bwd) on a small
+    ragged shape, so the full-coverage comparison below is anchored to it."""
+    import torch
+    torch.backends.cuda.matmul.allow_tf32 = False
+    f, s, d, B = 6, 300, 128, 128
+    n = f * s
+    rng = np.random.default_rng(9)
+    q, k, v, do = (O.bf16_round(rng.standard_normal((n, d)).astype(np.float32)) for _ in range(4))
+    lay = P.device_layout(P.GridShape(f, s), P.PatternSpec.radial(), B)
+    host = lay.host()
+    R = host.grid_rows
+    idx, lens = _padded_lists(host.row_ptr, host.col_idx, R, "cuda")
+    t = lambda x: torch.from_numpy(x).cuda().to(torch.bfloat16)
+    got = fp32_blockwise_bwd(t(q), t(k), t(v), t(do), idx, lens, B, n, 1.0 / np.sqrt(d))
+    want = O.attention_bwd(q, k, v, do, B, host.row_ptr, host.col_idx)
+    for g, w in zip(got, want):
+        assert np.abs(g[:n].cpu().numpy() - w).max() < 1e-4
+
+
+def _full_coverage_bwd(P, f, s, H, seed):
+    import torch
+    torch.backends.cuda.matmul.allow_tf32 = False
+    B, d = 128, 128
+    n = f * s
+    scale = 1.0 / np.sqrt(d)
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    q, k, v, do = (torch.randn(H, n, d, device="cuda", generator=g).to(torch.bfloat16) for _ in range(4))
+    lay = P.device_layout(P.GridShape(f, s), P.PatternSpec.radial(), B)
+    o, lse = P.masked_attention(q, k, v, lay, return_lse=True)
+    dq, dk, dv = P.masked_attention_backward(q, k, v, o, lse, do, lay)
+    torch.cuda.synchronize()
+    host = lay.host()
+    R = host.grid_rows
+    idx, lens = _padded_lists(host.row_ptr, host.col_idx, R, q.device)
+    worst = {"dQ": 0.0, "dK": 0.0, "dV": 0.0}
+    for h in range(H):
+        wants = fp32_blockwise_bwd(q[h], k[h], v[h], do[h], idx, lens, B, n, scale)
+        for name, got, want in zip(("dQ", "dK", "dV"), (dq[h], dk[h], dv[h]), wants):
+            gotp = torch.nn.functional.pad(got.float(), (0, 0, 0, R * B - n))
+            _, rel = _per_block_errors(gotp, want, B)
+            glob = float(torch.linalg.vector_norm(gotp - want) / torch.linalg.vector_norm(want))
+            worst[name] = max(worst[name], float(rel.max()))
+            assert float(rel.max()) <= 1e-2 and glob <= 6e-3, (
+                f"f{f} head {h} {name}: block {int(rel.argmax())} rel-L2 {float(rel.max()):.3e}, global {glob:.3e}")
+    del q, k, v, do, o, lse, dq, dk, dv
+    torch.cuda.empty_cache()
+    return worst
+
+
+def test_backward_full_coverage_mochi28(P):
+    """BASELINE configs[3] (the fwd + bwd LoRA path): dQ of every (head, query block) and dK / dV
+    of every (head, KV block), 24 x 348 each, against the fp32 restatement."""
+    w = _full_coverage_bwd(P, 28, 1590, 24, seed=28)
+    print("M28 backward full coverage, worst per-block rel-L2:", {k: f"{v:.3e}" for k, v in w.items()})
+
+
+def test_backward_full_coverage_hunyuan33(P):
+    """The headline shape: every (head, block) of dQ, dK, dV at H33 (24 x 929 each)."""
+    w = _full_coverage_bwd(P, 33, 3600, 24, seed=33)
+    print("H33 backward full coverage, worst per-block rel-L2:", {k: f"{v:.3e}" for k, v in w.items()})

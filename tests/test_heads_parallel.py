@@ -114,5 +114,5 @@ def test_bench_shared_gpu_runs_the_multi_rank_path():
                 "--no-extra", "--no-bwd", "--no-dense"])
     assert r.returncode == 0, r.stderr[-3000:]
     line = json.loads(r.stdout.strip().splitlines()[-1])
-    assert line["n_gpus"] == 2 and line["config"]["heads_per_rank"] == [[0, 12], [12, 24]]
+    assert line["n_gpus"] == 2 and line["config"]["heads_per_rank"] == [12, 12]
     assert "shared_gpu_plumbing_test" in line and line["gpu_launches"] >= 4
