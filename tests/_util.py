@@ -79,3 +79,26 @@ def bf16_pipeline_bwd(q, k, v, do, B, row_ptr, col_idx):
     p_b = O.bf16_round(p32.astype(np.float32)).astype(np.float64)
     ds_b = O.bf16_round(ds.astype(np.float32)).astype(np.float64)
     return (ds_b @ k64) * sc, (ds_b.T @ q64) * sc, p_b.T @ do64
+
+
+def radial_token_keep(rows, keys, s, sink=True):
+    """The reference token rule for the radial kind (mask.hpp:105-154 kept_span with
+    k_lo = k_hi = k, plus the sink of mask.hpp:120), vectorised: bool of broadcast(rows, keys)
+    global token indices."""
+    import torch
+    i, k = rows // s, rows % s
+    j, l = keys // s, keys % s
+    d = (i - j).abs()
+    e = torch.where(d <= 1, torch.zeros_like(d), torch.floor(torch.log2(d.clamp_min(1).double())).long())
+    # floor(log2 d) from a double: correct a rounding to either side
+    e = e - ((1 << e) > d).long() * (d > 1).long()
+    e = e + ((1 << (e + 1)) <= d).long() * (d > 1).long()
+    pw = 1 << e
+    band = pw <= s
+    sigma = (s >> e.clamp_max(62)) - 1
+    keep = band & ((k - l).abs() <= sigma)
+    period = (pw + s - 1) // s
+    keep = keep | (~band & (l == k) & (d % period == 0))
+    if sink:
+        keep = keep | (j == 0)
+    return keep

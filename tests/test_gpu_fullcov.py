@@ -17,7 +17,7 @@ import numpy as np
 import pytest
 
 import oracle as O
-from tests._util import MAX_ABS, REL_L2, assert_within, block_errors
+from tests._util import MAX_ABS, REL_L2, assert_within, block_errors, radial_token_keep
 
 pytestmark = pytest.mark.gpu
 
@@ -44,7 +44,7 @@ def _padded_lists(row_ptr, col_idx, R, device):
     return idx, lens
 
 
-def fp32_blockwise(q, k, v, idx, lens, B, n, scale, blocks=None, rows_per_batch=None):
+def fp32_blockwise(q, k, v, idx, lens, B, n, scale, blocks=None, rows_per_batch=None, token_keep=None):
     """fp32 restatement of attention.hpp:238-268 for one head, query blocks `blocks` (all by
     default): O [len(blocks) * B, d] (rows >= n are zero) and lse [len(blocks) * B].
     q/k/v: bf16 [n, d] on the GPU; idx: padded kept-block lists (pad = R)."""
@@ -69,6 +69,9 @@ def fp32_blockwise(q, k, v, idx, lens, B, n, scale, blocks=None, rows_per_batch=
         key = (ib[:, :, None] * B + ar).reshape(bl.numel(), 1, L * B)
         ok = (ib[:, :, None] < R).expand(-1, -1, B).reshape(bl.numel(), 1, L * B) & (key < n)
         s = torch.bmm(qf[bl], kg.transpose(1, 2)) * scale           # [nb, B, L*B]
+        if token_keep is not None:
+            qrow = (bl[:, None] * B + ar).reshape(bl.numel(), B, 1)
+            ok = ok & token_keep(qrow, key)
         s = s.masked_fill(~ok, float("-inf"))
         m = s.amax(dim=2, keepdim=True)
         p = torch.exp(s - m)
@@ -295,3 +298,44 @@ def test_backward_full_coverage_hunyuan33(P):
     """The headline shape: every (head, block) of dQ, dK, dV at H33 (24 x 929 each)."""
     w = _full_coverage_bwd(P, 33, 3600, 24, seed=33)
     print("H33 backward full coverage, worst per-block rel-L2:", {k: f"{v:.3e}" for k, v in w.items()})
+
+
+# ------------------------------------------------------------------------------ token-exact
+def test_token_exact_full_coverage_hunyuan33(P):
+    """masked_attention(inst, PatternSpec) (attention.hpp:184-225) at the
+    headline shape: every (head, query block) against the fp32 restatement over the radial block
+    layout with the reference token rule applied inside each block; the restatement is pinned to
+    the fp64 token oracle on sampled rows."""
+    import torch
+    torch.backends.cuda.matmul.allow_tf32 = False
+    f, s, H, B, d = 33, 3600, 24, 128, 128
+    n = f * s
+    scale = 1.0 / np.sqrt(d)
+    g = torch.Generator(device="cuda").manual_seed(8)
+    q, k, v = (torch.randn(H, n, d, device="cuda", generator=g).to(torch.bfloat16) for _ in range(3))
+    o = P.masked_attention_pattern(q, k, v, P.GridShape(f, s), P.PatternSpec.radial(), block_size=B)
+    torch.cuda.synchronize()
+    lay = P.device_layout(P.GridShape(f, s), P.PatternSpec.radial(), B)
+    host = lay.host()
+    R = host.grid_rows
+    idx, lens = _padded_lists(host.row_ptr, host.col_idx, R, q.device)
+    keep = lambda rows, keys: radial_token_keep(rows, keys, s, sink=True)
+    worst_abs = worst_rel = 0.0
+    for h in range(H):
+        want, _ = fp32_blockwise(q[h], k[h], v[h], idx, lens, B, n, scale, token_keep=keep,
+                                 rows_per_batch=4)
+        got = torch.nn.functional.pad(o[h].float(), (0, 0, 0, R * B - n))
+        valid = torch.arange(R * B, device=q.device) < n
+        want = want * valid[:, None]
+        mx, rel = _per_block_errors(got, want, B)
+        worst_abs, worst_rel = max(worst_abs, float(mx.max())), max(worst_rel, float(rel.max()))
+        assert float(mx.max()) <= MAX_ABS and float(rel.max()) <= REL_L2, (
+            f"head {h}: block {int(rel.argmax())} rel-L2 {float(rel.max()):.3e}, max-abs {float(mx.max()):.3e}")
+        if h == 0:
+            rng = np.random.default_rng(3)
+            rows = np.sort(rng.choice(n, 300, replace=False))
+            qh, kh, vh = (x[h].float().cpu().numpy() for x in (q, k, v))
+            ref = O.token_attention_rows(qh, kh, vh, f, s, rows)
+            mine = want[torch.from_numpy(rows).to(q.device)].cpu().numpy()
+            assert np.abs(mine - ref).max() < 1e-4, "fp32 token restatement disagrees with the fp64 oracle"
+    print(f"H33 token-exact full coverage: worst per-block max-abs {worst_abs:.3e}, rel-L2 {worst_rel:.3e}")

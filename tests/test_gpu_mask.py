@@ -89,3 +89,18 @@ def test_layout_from_host_csr_roundtrip_and_validation(P):
     bad.col_idx[1] = bad.col_idx[0]
     with pytest.raises(ValueError, match="strictly increasing"):
         P.layout_from_host(bad)
+
+
+@pytest.mark.skipif(not O.ref_available(), reason="oracle/_ref not built")
+@pytest.mark.parametrize("f,s", [(33, 3600), (28, 1590)])
+def test_device_blockify_all_kinds_paper_scale_vs_reference(P, f, s):
+    """K1 for every pattern kind at the BASELINE shapes, byte-identical with the reference's
+    own blockify + serialize (oracle/_ref, the unmodified reference headers)."""
+    B = 128
+    specs = [(P.PatternSpec.dense(), "dense", 0, 0), (P.PatternSpec.sta(2, 600), "sta", 2, 600),
+             (P.PatternSpec.temporal(300, True), "temporal", 0, 300), (P.PatternSpec.spatial(2), "spatial", 2, 0),
+             (P.PatternSpec.harmonic(True), "harmonic", 0, 0), (P.PatternSpec.power(True), "power", 0, 0),
+             (P.PatternSpec.radial(False), "radial", 0, 0)]
+    for spec, kind, tw, sw in specs:
+        mine = P.serialize(P.blockify(P.GridShape(f, s), spec, B))
+        assert mine == O.ref_serialize(f, s, B, kind, spec.sink, tw, sw), (f, s, kind)

@@ -184,3 +184,20 @@ def test_token_attention_rows_match_reference_every_kind(kind, sink, tw, sw):
     ref = O.ref_masked_attention_pattern(f, s, q, k, v, kind, sink, tw, sw)
     mine = O.token_attention_rows(q, k, v, f, s, np.arange(f * s), kind, sink, tw, sw)
     assert np.abs(mine - ref).max() < 1e-12
+
+
+def test_vectorised_radial_token_rule_matches_oracle():
+    """tests._util.radial_token_keep (used by the GPU full-coverage token-exact test) equals the
+    oracle's radial_keep, which test_radial_keep_exhaustive_vs_reference pins to the reference;
+    random (i, j, k, l) including far frames where 2^e > s (the diagonal case)."""
+    import torch
+    from tests._util import radial_token_keep
+    lib = O.c()
+    rng = np.random.default_rng(11)
+    for s, f in ((3600, 33), (5, 600), (1, 300), (7, 9)):
+        i, j = rng.integers(0, f, 4000), rng.integers(0, f, 4000)
+        k, l = rng.integers(0, s, 4000), rng.integers(0, s, 4000)
+        for sink in (True, False):
+            got = radial_token_keep(torch.from_numpy(i * s + k), torch.from_numpy(j * s + l), s, sink).numpy()
+            want = [bool(lib.ro_radial_keep(int(a), int(b), int(c), int(e), s, int(sink))) for a, b, c, e in zip(i, j, k, l)]
+            assert got.tolist() == want, (s, f, sink)
