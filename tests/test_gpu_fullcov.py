@@ -166,6 +166,13 @@ def test_full_coverage_hunyuan132(P):
     print(f"H132 full coverage: worst per-block max-abs {wa:.3e}, rel-L2 {wr:.3e}")
 
 
+@pytest.mark.parametrize("f,s,H", [(21, 3600, 40), (28, 1590, 24)], ids=["wan21", "mochi28"])
+def test_full_coverage_other_configs(P, f, s, H):
+    """BASELINE configs[2] and [3]: every (head, query block) pair of the forward."""
+    wa, wr = _full_coverage(P, f, s, H, seed=f * 100 + H)
+    print(f"f{f} s{s} full coverage: worst per-block max-abs {wa:.3e}, rel-L2 {wr:.3e}")
+
+
 def test_dense_comparator_hunyuan33_sampled(P):
     """K4 at the headline H33 shape (118,800 keys per row) on sampled query blocks of every
     head, against the fp32 dense restatement (dense_attention, attention.hpp:141-163)."""
