@@ -100,6 +100,10 @@ constexpr int kPolyPairs = RADIAL_POLY_PAIRS;  // column pairs per 8 using the p
 
 constexpr int kMaxDst = 8;  // fused all-gather: O rows stored into up to 8 ranks' buffers
 
+#ifndef RADIAL_FWD_L2HINTS
+#define RADIAL_FWD_L2HINTS 1  // L2 eviction hints: Q evict-first, K/V evict-last, O streaming stores
+#endif
+
 #ifndef RADIAL_TOK_PAIRED
 #define RADIAL_TOK_PAIRED 0
 #endif
@@ -239,11 +243,20 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (warp == 0) {
         // ------------------------------------------------------------ producer
         if (lane == 0) {
+#if RADIAL_FWD_L2HINTS
+            const uint64_t pol_first = l2_policy_evict_first(), pol_last = l2_policy_evict_last();
+#endif
             mbar_arrive_expect_tx(bar_q, 2 * Cfg::kQBytes);
             for (int t = 0; t < 2; ++t)
                 for (int a = 0; a < Cfg::kAtoms; ++a)
+#if RADIAL_FWD_L2HINTS
+                    // Q is read once: evict-first keeps the L2 for the K/V tiles every chunk re-reads
+                    tma_load_3d_hint(smem + Cfg::kSmemQ + t * Cfg::kQBytes + a * Cfg::kQAtomBytes, &tm_q,
+                                     bar_q, a * 64, static_cast<int32_t>(row0 + t * kBQ), head, pol_first);
+#else
                     tma_load_3d(smem + Cfg::kSmemQ + t * Cfg::kQBytes + a * Cfg::kQAtomBytes, &tm_q,
                                 bar_q, a * 64, static_cast<int32_t>(row0 + t * kBQ), head);
+#endif
             for (uint32_t t = 0; t < 2 * L; ++t) {
                 const int32_t J = static_cast<int32_t>(entry(t >> 1) & 0x0FFFFFFFu);
                 const uint32_t slot = t % kSlots;
@@ -257,7 +270,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                 uint8_t* dst = smem + Cfg::kSmemKV + slot * Cfg::kKVBytes;
                 const CUtensorMap* tm = (t & 1) ? &tm_v : &tm_k;
                 for (int a = 0; a < Cfg::kAtoms; ++a)
+#if RADIAL_FWD_L2HINTS
+                    tma_load_3d_hint(dst + a * Cfg::kKVAtomBytes, tm, &bar_full[slot], a * 64, J * BK, head, pol_last);
+#else
                     tma_load_3d(dst + a * Cfg::kKVAtomBytes, tm, &bar_full[slot], a * 64, J * BK, head);
+#endif
             }
         }
     } else if (warp == 1) {
@@ -722,7 +739,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (p.n_dst == 0) {
                     uint4* dst = reinterpret_cast<uint4*>(orow + c);
 #pragma unroll
-                    for (int x = 0; x < 4; ++x) dst[x] = make_uint4(w[4 * x], w[4 * x + 1], w[4 * x + 2], w[4 * x + 3]);
+                    for (int x = 0; x < 4; ++x) {
+#if RADIAL_FWD_L2HINTS
+                        __stcs(dst + x, make_uint4(w[4 * x], w[4 * x + 1], w[4 * x + 2], w[4 * x + 3]));  // streaming
+#else
+                        dst[x] = make_uint4(w[4 * x], w[4 * x + 1], w[4 * x + 2], w[4 * x + 3]);
+#endif
+                    }
                 } else {
                     // every rank's full O: stores to peer GPUs go straight over NVLink while the
                     // other CTAs are still computing (no all-gather after the kernel)
