@@ -51,6 +51,15 @@ __device__ unsigned long long* g_btrace = nullptr;
     } while (0)
 #endif
 
+#ifndef RADIAL_BWD_L2HINTS
+#define RADIAL_BWD_L2HINTS 0  // L2 eviction hints (tiles read once evict-first, re-read tiles evict-last): measured neutral, off
+#endif
+#if RADIAL_BWD_L2HINTS
+#define BWD_LOAD(dst, map, bar, c0, c1, c2, pol) tma_load_3d_hint(dst, map, bar, c0, c1, c2, pol)
+#else
+#define BWD_LOAD(dst, map, bar, c0, c1, c2, pol) tma_load_3d(dst, map, bar, c0, c1, c2)
+#endif
+
 namespace {
 
 constexpr int kThreads = 384;   // warp0 TMA, warp1 MMA, warp2 TMEM alloc, warps 4-11 elementwise
@@ -193,21 +202,24 @@ __global__ void __launch_bounds__(kThreads, 1)
         regs_dec<RADIAL_REGS_LO>();
         if (warp == 0 && lane == 0) {
             // ------------------------------------------------ producer
+            // dO_I is read once (evict-first); K_j / V_j are re-read by every query block of
+            // their CSC column (evict-last)
+            [[maybe_unused]] const uint64_t pol_first = l2_policy_evict_first(), pol_last = l2_policy_evict_last();
             mbar_arrive_expect_tx(bar_do, T);
             for (int a = 0; a < Cfg::kAtoms; ++a)
-                tma_load_3d(smem + a * Cfg::kAtomBytes, &tm_do, bar_do, a * 64, I * kBlk, head);
+                BWD_LOAD(smem + a * Cfg::kAtomBytes, &tm_do, bar_do, a * 64, I * kBlk, head, pol_first);
             for (uint32_t j = 0; j < L; ++j) {
                 const int32_t J = static_cast<int32_t>(__ldg(p.idx + e0 + j));
                 const int ks = j % kKS, vs = j % kVS;
                 mbar_wait(&bar_kempty[ks], ((j / kKS) & 1) ^ 1);
                 mbar_arrive_expect_tx(&bar_kfull[ks], T);
                 for (int a = 0; a < Cfg::kAtoms; ++a)
-                    tma_load_3d(smem + (1 + ks) * T + a * Cfg::kAtomBytes, &tm_k, &bar_kfull[ks], a * 64, J * kBlk, head);
+                    BWD_LOAD(smem + (1 + ks) * T + a * Cfg::kAtomBytes, &tm_k, &bar_kfull[ks], a * 64, J * kBlk, head, pol_last);
                 mbar_wait(&bar_vempty[vs], ((j / kVS) & 1) ^ 1);
                 mbar_arrive_expect_tx(&bar_vfull[vs], T);
                 for (int a = 0; a < Cfg::kAtoms; ++a)
-                    tma_load_3d(smem + (1 + kKS + vs) * T + a * Cfg::kAtomBytes, &tm_v, &bar_vfull[vs], a * 64,
-                                J * kBlk, head);
+                    BWD_LOAD(smem + (1 + kKS + vs) * T + a * Cfg::kAtomBytes, &tm_v, &bar_vfull[vs], a * 64,
+                                J * kBlk, head, pol_last);
             }
         } else if (warp == 1) {  // whole warp, converged (elected issue)
             // ------------------------------------------------ MMA issuer
@@ -485,10 +497,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         regs_dec<RADIAL_REGS_LO>();
         if (warp == 0 && lane == 0) {
             // ------------------------------------------------ producer
+            // K_J / V_J are read once (evict-first); Q_I / dO_I are re-read by every KV block
+            // of their CSR row (evict-last)
+            [[maybe_unused]] const uint64_t pol_first = l2_policy_evict_first(), pol_last = l2_policy_evict_last();
             mbar_arrive_expect_tx(bar_res, 2 * T);
             for (int a = 0; a < Cfg::kAtoms; ++a) {
-                tma_load_3d(smem + a * Cfg::kAtomBytes, &tm_k, bar_res, a * 64, J * kBlk, head);
-                tma_load_3d(smem + T + a * Cfg::kAtomBytes, &tm_v, bar_res, a * 64, J * kBlk, head);
+                BWD_LOAD(smem + a * Cfg::kAtomBytes, &tm_k, bar_res, a * 64, J * kBlk, head, pol_first);
+                BWD_LOAD(smem + T + a * Cfg::kAtomBytes, &tm_v, bar_res, a * 64, J * kBlk, head, pol_first);
             }
             for (uint32_t i = 0; i < L; ++i) {
                 const int qs = i % kQS, ds = i % kDS;
@@ -496,14 +511,14 @@ __global__ void __launch_bounds__(kThreads, 1)
                 mbar_wait(&bar_qempty[qs], ((i / kQS) & 1) ^ 1);
                 mbar_arrive_expect_tx(&bar_qfull[qs], T);
                 for (int a = 0; a < Cfg::kAtoms; ++a)
-                    tma_load_3d(smem + kOffQ + qs * T + a * Cfg::kAtomBytes, &tm_q, &bar_qfull[qs], a * 64,
-                                Iq * kBlk, head);
+                    BWD_LOAD(smem + kOffQ + qs * T + a * Cfg::kAtomBytes, &tm_q, &bar_qfull[qs], a * 64,
+                                Iq * kBlk, head, pol_last);
                 mbar_wait(&bar_doempty[ds], ((i / kDS) & 1) ^ 1);
                 mbar_wait(&bar_vecempty[ds], ((i / kDS) & 1) ^ 1);
                 mbar_arrive_expect_tx(&bar_dofull[ds], T + 2 * kBlk * 4);
                 for (int a = 0; a < Cfg::kAtoms; ++a)
-                    tma_load_3d(smem + kOffDO + ds * T + a * Cfg::kAtomBytes, &tm_do, &bar_dofull[ds], a * 64,
-                                Iq * kBlk, head);
+                    BWD_LOAD(smem + kOffDO + ds * T + a * Cfg::kAtomBytes, &tm_do, &bar_dofull[ds], a * 64,
+                                Iq * kBlk, head, pol_last);
                 const uint64_t off = static_cast<uint64_t>(head) * p.rpad + static_cast<uint64_t>(Iq) * kBlk;
                 bulk_load(vec + ds * 256, p.lse2 + off, kBlk * 4, &bar_dofull[ds]);
                 bulk_load(vec + ds * 256 + 128, p.dvec + off, kBlk * 4, &bar_dofull[ds]);
