@@ -51,6 +51,12 @@ __device__ unsigned long long* g_btrace = nullptr;
     } while (0)
 #endif
 
+#ifndef RADIAL_BWD_DQ_POLY
+#define RADIAL_BWD_DQ_POLY 1  // column pairs per 8 whose exp2 runs on the FMA pipe in the dQ kernel (measured best)
+#endif
+#ifndef RADIAL_BWD_DKDV_POLY
+#define RADIAL_BWD_DKDV_POLY 0  // column quads per 4 whose exp2 runs on the FMA pipe in the dK/dV kernel
+#endif
 #ifndef RADIAL_BWD_L2HINTS
 #define RADIAL_BWD_L2HINTS 0  // L2 eviction hints (tiles read once evict-first, re-read tiles evict-last): measured neutral, off
 #endif
@@ -350,8 +356,16 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int c = 0; c < 64; c += 2) {
                 const float2 x = __ffma2_rn(make_float2(__uint_as_float(sv[c]), __uint_as_float(sv[c + 1])), sl, nl);
-                pv[c] = ex2(x.x);
-                pv[c + 1] = ex2(x.y);
+                if (((c >> 1) & 7) < RADIAL_BWD_DQ_POLY) {
+                    // a share of the exponentials on the FMA pipe: this loop's chain is bound by
+                    // the MUFU queue (two warps x 64 ex2 per sub-partition), not by issue slots
+                    const float2 pr = ex2_poly2(x);
+                    pv[c] = pr.x;
+                    pv[c + 1] = pr.y;
+                } else {
+                    pv[c] = ex2(x.x);
+                    pv[c + 1] = ex2(x.y);
+                }
             }
             if (valid < 64) {
 #pragma unroll
@@ -631,10 +645,18 @@ __global__ void __launch_bounds__(kThreads, 1)
                                              sl, make_float2(-l4.x, -l4.y));
                 const float2 xb = __ffma2_rn(make_float2(__uint_as_float(sv[4 * c4 + 2]), __uint_as_float(sv[4 * c4 + 3])),
                                              sl, make_float2(-l4.z, -l4.w));
-                pv[4 * c4 + 0] = ex2(xa.x);
-                pv[4 * c4 + 1] = ex2(xa.y);
-                pv[4 * c4 + 2] = ex2(xb.x);
-                pv[4 * c4 + 3] = ex2(xb.y);
+                if ((c4 & 3) < RADIAL_BWD_DKDV_POLY) {  // a share of the exp2 on the FMA pipe
+                    const float2 pa = ex2_poly2(xa), pb = ex2_poly2(xb);
+                    pv[4 * c4 + 0] = pa.x;
+                    pv[4 * c4 + 1] = pa.y;
+                    pv[4 * c4 + 2] = pb.x;
+                    pv[4 * c4 + 3] = pb.y;
+                } else {
+                    pv[4 * c4 + 0] = ex2(xa.x);
+                    pv[4 * c4 + 1] = ex2(xa.y);
+                    pv[4 * c4 + 2] = ex2(xb.x);
+                    pv[4 * c4 + 3] = ex2(xb.y);
+                }
             }
             if ((warp == 4 || warp == 8) && lane == 0) BTRACE(warp == 4 ? 7 : 10, i);
             mbar_wait(bar_dp, i & 1);

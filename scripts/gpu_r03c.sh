@@ -1,0 +1,4 @@
+tag=r03c
+mkdir -p gpurun_out
+timeout 1500 python -m pytest tests/test_gpu_backward.py tests/test_gpu_fullcov.py -q -s -p no:cacheprovider -k "backward" > gpurun_out/${tag}_pytest.log 2>&1
+echo "pytest rc=$?" >> gpurun_out/${tag}_pytest.log
