@@ -96,10 +96,9 @@ def _per_block_errors(got, want, B, ulp_slack=False):
     return mx, rel
 
 
-def _full_coverage(P, f, s, H, q_scale=1.0, seed=4321, pin_heads=(0,)):
+def _full_coverage(P, f, s, H, q_scale=1.0, seed=4321, pin_heads=(0,), B=128, d=128):
     import torch
     torch.backends.cuda.matmul.allow_tf32 = False
-    B, d = 128, 128
     n = f * s
     scale = 1.0 / np.sqrt(d)
     g = torch.Generator(device="cuda").manual_seed(seed)
@@ -171,6 +170,14 @@ def test_full_coverage_other_configs(P, f, s, H):
     """BASELINE configs[2] and [3]: every (head, query block) pair of the forward."""
     wa, wr = _full_coverage(P, f, s, H, seed=f * 100 + H)
     print(f"f{f} s{s} full coverage: worst per-block max-abs {wa:.3e}, rel-L2 {wr:.3e}")
+
+
+@pytest.mark.parametrize("B,d", [(64, 128), (64, 64), (128, 64)])
+def test_full_coverage_other_tile_shapes_mochi28(P, B, d):
+    """The other K2 instantiations (block 64 and / or head_dim 64) at the M28 shape, every
+    (head, query block) pair."""
+    wa, wr = _full_coverage(P, 28, 1590, 24, seed=B * 1000 + d, B=B, d=d)
+    print(f"M28 B{B} d{d} full coverage: worst per-block max-abs {wa:.3e}, rel-L2 {wr:.3e}")
 
 
 def test_dense_comparator_hunyuan33_sampled(P):
