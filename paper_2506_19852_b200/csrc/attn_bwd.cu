@@ -54,6 +54,15 @@ __device__ unsigned long long* g_btrace = nullptr;
 #ifndef RADIAL_BWD_DQ_POLY
 #define RADIAL_BWD_DQ_POLY 1  // column pairs per 8 whose exp2 runs on the FMA pipe in the dQ kernel (measured best)
 #endif
+#ifndef RADIAL_BWD_DQ_SPLIT_S
+#define RADIAL_BWD_DQ_SPLIT_S 0  // dQ kernel: load S in two 32-column halves, the second under the first's exps
+#endif
+#ifndef RADIAL_BWD_DQ_EARLY_DP
+#define RADIAL_BWD_DQ_EARLY_DP 48  // dQ kernel: column index at which dP is loaded under the exponentials (0 = after)
+#endif
+#ifndef RADIAL_BWD_DKDV_EARLY_DP
+#define RADIAL_BWD_DKDV_EARLY_DP 0  // dK/dV kernel: column at which dP^T is loaded under the exponentials
+#endif
 #ifndef RADIAL_BWD_DKDV_POLY
 #define RADIAL_BWD_DKDV_POLY 0  // column quads per 4 whose exp2 runs on the FMA pipe in the dK/dV kernel
 #endif
@@ -339,22 +348,41 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (warp == 4 && lane == 0) BTRACE(5, j);
             tc_fence_after();
             uint32_t sv[64];
-#ifdef RADIAL_BWD_LD32
-            tmem_ld32(kTmem + la + kColS + wg * 64, *reinterpret_cast<uint32_t(*)[32]>(sv));
-            tmem_ld32(kTmem + la + kColS + wg * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(sv + 32));
-#else
-            tmem_ld64(kTmem + la + kColS + wg * 64, sv);
-#endif
-            tmem_wait_ld();
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(bar_sfree);
+            uint32_t dp[64];
             const uint64_t key0 = static_cast<uint64_t>(J) * kBlk + wg * 64;
             const int valid = key0 + 64 <= p.n ? 64 : (key0 < p.n ? static_cast<int>(p.n - key0) : 0);
             float pv[64];
             const float2 sl = make_float2(sl2, sl2), nl = make_float2(-lse2, -lse2);
+#if RADIAL_BWD_DQ_SPLIT_S
+            // the first 32 columns, then the second half's load runs under their exponentials
+            tmem_ld32(kTmem + la + kColS + wg * 64, *reinterpret_cast<uint32_t(*)[32]>(sv));
+            tmem_wait_ld();
+            tmem_ld32(kTmem + la + kColS + wg * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(sv + 32));
+#else
+            tmem_ld64(kTmem + la + kColS + wg * 64, sv);
+            tmem_wait_ld();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(bar_sfree);
+#endif
 #pragma unroll
             for (int c = 0; c < 64; c += 2) {
+#if RADIAL_BWD_DQ_SPLIT_S
+                if (c == 32) {
+                    tmem_wait_ld();
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(bar_sfree);
+                }
+#endif
+#if RADIAL_BWD_DQ_EARLY_DP
+                if (c == RADIAL_BWD_DQ_EARLY_DP) {
+                    // dP(j) (computed right after S(j)) is loaded under the last exponentials
+                    mbar_wait(bar_dp, j & 1);
+                    tc_fence_after();
+                    tmem_ld64(kTmem + la + kColDP + wg * 64, dp);
+                }
+#endif
                 const float2 x = __ffma2_rn(make_float2(__uint_as_float(sv[c]), __uint_as_float(sv[c + 1])), sl, nl);
                 if (((c >> 1) & 7) < RADIAL_BWD_DQ_POLY) {
                     // a share of the exponentials on the FMA pipe: this loop's chain is bound by
@@ -371,14 +399,15 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                 for (int c = 0; c < 64; ++c) pv[c] = c < valid ? pv[c] : 0.f;
             }
+#if !RADIAL_BWD_DQ_EARLY_DP
             mbar_wait(bar_dp, j & 1);
             tc_fence_after();
-            uint32_t dp[64];
 #ifdef RADIAL_BWD_LD32
             tmem_ld32(kTmem + la + kColDP + wg * 64, *reinterpret_cast<uint32_t(*)[32]>(dp));
             tmem_ld32(kTmem + la + kColDP + wg * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(dp + 32));
 #else
             tmem_ld64(kTmem + la + kColDP + wg * 64, dp);
+#endif
 #endif
             tmem_wait_ld();
             tc_fence_before();
@@ -638,8 +667,16 @@ __global__ void __launch_bounds__(kThreads, 1)
             const float4* lv = reinterpret_cast<const float4*>(vec + ds * 256 + wg * 64);
             float pv[64];
             const float2 sl = make_float2(sl2, sl2);
+            uint32_t dp[64];
 #pragma unroll
             for (int c4 = 0; c4 < 16; ++c4) {
+#if RADIAL_BWD_DKDV_EARLY_DP
+                if (c4 == RADIAL_BWD_DKDV_EARLY_DP / 4) {  // dP^T(i) loaded under the last exponentials
+                    mbar_wait(bar_dp, i & 1);
+                    tc_fence_after();
+                    tmem_ld64(kTmem + la + kColDP + wg * 64, dp);
+                }
+#endif
                 const float4 l4 = lv[c4];
                 const float2 xa = __ffma2_rn(make_float2(__uint_as_float(sv[4 * c4]), __uint_as_float(sv[4 * c4 + 1])),
                                              sl, make_float2(-l4.x, -l4.y));
@@ -659,15 +696,16 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
             }
             if ((warp == 4 || warp == 8) && lane == 0) BTRACE(warp == 4 ? 7 : 10, i);
+#if !RADIAL_BWD_DKDV_EARLY_DP
             mbar_wait(bar_dp, i & 1);
             if (warp == 4 && lane == 0) BTRACE(8, i);
             tc_fence_after();
-            uint32_t dp[64];
 #ifdef RADIAL_BWD_LD32
             tmem_ld32(kTmem + la + kColDP + wg * 64, *reinterpret_cast<uint32_t(*)[32]>(dp));
             tmem_ld32(kTmem + la + kColDP + wg * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(dp + 32));
 #else
             tmem_ld64(kTmem + la + kColDP + wg * 64, dp);
+#endif
 #endif
             tmem_wait_ld();
             // P^T into the (now consumed) dP^T columns, in two query halves
