@@ -64,7 +64,7 @@ __device__ unsigned long long* g_btrace = nullptr;
 #define RADIAL_BWD_DKDV_EARLY_DP 0  // dK/dV kernel: column at which dP^T is loaded under the exponentials
 #endif
 #ifndef RADIAL_BWD_DKDV_POLY
-#define RADIAL_BWD_DKDV_POLY 0  // column quads per 4 whose exp2 runs on the FMA pipe in the dK/dV kernel
+#define RADIAL_BWD_DKDV_POLY 0  // column quads per 8 whose exp2 runs on the FMA pipe in the dK/dV kernel
 #endif
 #ifndef RADIAL_BWD_L2HINTS
 #define RADIAL_BWD_L2HINTS 0  // L2 eviction hints (tiles read once evict-first, re-read tiles evict-last): measured neutral, off
@@ -682,7 +682,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                                              sl, make_float2(-l4.x, -l4.y));
                 const float2 xb = __ffma2_rn(make_float2(__uint_as_float(sv[4 * c4 + 2]), __uint_as_float(sv[4 * c4 + 3])),
                                              sl, make_float2(-l4.z, -l4.w));
-                if ((c4 & 3) < RADIAL_BWD_DKDV_POLY) {  // a share of the exp2 on the FMA pipe
+                if ((c4 & 7) < RADIAL_BWD_DKDV_POLY) {  // a share of the exp2 on the FMA pipe
                     const float2 pa = ex2_poly2(xa), pb = ex2_poly2(xb);
                     pv[4 * c4 + 0] = pa.x;
                     pv[4 * c4 + 1] = pa.y;
