@@ -134,3 +134,16 @@ def test_mask_build_rejects_missing_windows(kind, tw, sw, msg):
     assert rc == P.ERR_INVALID
     assert P._lib.radial_cuda_last_error().decode() == msg
     assert not h.value
+
+
+def test_missing_cuda_library_fails_loudly(tmp_path):
+    """No CPU fallback: importing the package without its CUDA library raises ImportError
+    (a fresh interpreter, pointed at a path that does not exist)."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, RADIAL_CUDA_LIB=str(tmp_path / "missing" / "libradial_cuda.so"))
+    r = subprocess.run([sys.executable, "-c", "import paper_2506_19852_b200"], cwd=root, env=env,
+                       capture_output=True, text=True, timeout=300)
+    assert r.returncode != 0
+    assert "ImportError" in r.stderr or "OSError" in r.stderr, r.stderr[-2000:]
